@@ -1,0 +1,688 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 fused-expression hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c4|c5]
+                    [--impl ours|reference]
+
+Default workload (the headline, BASELINE.json configs[1] = C2): one step is
+the six fused reductions accu(X % Y), dot(x, y), norm(x - y) over 1e8-element
+f32 AND f64 vectors per GPU, each a single launch of libfmb200.so.  `value`
+is device-timed whole-job GB/s (algorithmic bytes, the reference's
+plan_bytes convention, bench.py:218-240) with inputs resident in HBM;
+`e2e` is the same metric through the public API with the inputs uploaded
+from pinned host memory every step and the six results read back.
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling -- each rank owns a
+1e8-element slice of the global vectors (the splitmix64 stream at its
+offset); the six per-rank partials cross NVLink in ONE NCCL all_reduce per
+step.  Timing: barrier + device sync on both sides, CUDA events on the
+launching stream, max over ranks.
+
+`--impl reference` times the reference's own CPU path on the host cores:
+the C kernels its code generator emits (compiled by oracle/build_ref.py into
+oracle/_ref/) on a bounded sample, all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fused-expression effective HBM GB/s (% of 8 TB/s) and elements/s"
+SPEC_HBM_GBS = 8000.0
+FALLBACK_HBM_GBS = 6650.0
+FALLBACK_BF16_TFLOPS = 1590.0
+
+
+# --------------------------------------------------------------------------------------
+# helpers
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                    "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                    "source": "measured (MEASURED_PEAKS.json)"}
+        except Exception:
+            pass
+    return {"hbm_gbs": FALLBACK_HBM_GBS, "bf16_tflops": FALLBACK_BF16_TFLOPS,
+            "bf16_tflops_sustained": 1400.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic(kernel_key: str):
+    """dram read+write bytes per launch from the committed ncu capture."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        v = d.get(kernel_key)
+        if isinstance(v, dict):
+            return v.get("dram_bytes")
+        return v
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{self.local}"))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{self.local}")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{self.local}")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+class Events:
+    """CUDA events on the backend's stream (the stream the kernels run on)."""
+
+    def __init__(self, nat, stream, n):
+        self.nat, self.stream = nat, stream
+        self.ev = []
+        for _ in range(n):
+            e = ctypes.c_void_p()
+            nat.call("fm_event_create", ctypes.byref(e))
+            self.ev.append(e.value)
+
+    def record(self, i):
+        self.nat.call("fm_event_record", self.ev[i], self.stream)
+
+    def ms(self, i, j) -> float:
+        f = ctypes.c_float()
+        self.nat.call("fm_event_elapsed_ms", self.ev[i], self.ev[j], ctypes.byref(f))
+        return f.value
+
+
+# --------------------------------------------------------------------------------------
+# C2: fused reductions (the headline)
+class C2:
+    name = "c2"
+    workload = "C2 fused reductions accu(X%Y), dot(x,y), norm(x-y) on 1e8-element f32 and f64 vectors"
+
+    def __init__(self, args, d: Dist):
+        self.n = args.n or 100_000_000
+        self.d = d
+        self.labels = ["accu_schur_f32", "dot_f32", "norm_sqdiff_f32",
+                       "accu_schur_f64", "dot_f64", "norm_sqdiff_f64"]
+        self.kbytes = [2 * 4 * self.n + 8] * 3 + [2 * 8 * self.n + 8] * 3
+        self.unit = "GB/s"
+        self.dtype = "f32+f64 (f64 accumulation)"
+
+    def setup(self, fm, ctx):
+        n, off = self.n, self.d.rank * self.n
+        self.fm, self.ctx = fm, ctx
+        self.x32, self.y32 = fm.Col(n, "f32", ctx), fm.Col(n, "f32", ctx)
+        self.x64, self.y64 = fm.Col(n, "f64", ctx), fm.Col(n, "f64", ctx)
+        for m, seed in ((self.x32, 42), (self.y32, 43), (self.x64, 42), (self.y64, 43)):
+            ctx.backend.randu(m.handle, seed, offset=off)
+        self.R = fm.Mat(6, 1, "f64", ctx)
+        ctx.sync()
+
+    def launches(self):
+        """The six hot-path launches, as callables (one kernel each)."""
+        fm, x32, y32, x64, y64, R = self.fm, self.x32, self.y32, self.x64, self.y64, self.R
+        sq = self.d.world > 1
+        return [lambda: fm.accu_async(x32 % y32, R, 0), lambda: fm.dot_async(x32, y32, R, 1),
+                lambda: fm.norm_async(x32 - y32, R, 2, squared=sq),
+                lambda: fm.accu_async(x64 % y64, R, 3), lambda: fm.dot_async(x64, y64, R, 4),
+                lambda: fm.norm_async(x64 - y64, R, 5, squared=sq)]
+
+    def collective(self):
+        if self.d.world > 1:
+            from paper_2604_22242_b200.dist import torch_view
+            import torch
+            t = torch_view(self.ctx.backend, self.R.handle, self.d.local)
+            with torch.cuda.stream(torch.cuda.ExternalStream(self.ctx.backend.stream)):
+                self.d.pg.all_reduce(t)
+
+    def elements_per_step(self):
+        return 6 * self.n
+
+    def bytes_per_step(self):
+        return sum(self.kbytes)
+
+    def check(self):
+        """Sanity: results vs exact sums of the device data (sample)."""
+        r = self.R.to_numpy().ravel()
+        return {"accu_f32": r[0], "dot_f32": r[1], "norm_f32": r[2] if self.d.world == 1 else float(np.sqrt(r[2])),
+                "accu_f64": r[3], "dot_f64": r[4], "norm_f64": r[5] if self.d.world == 1 else float(np.sqrt(r[5]))}
+
+    # e2e: host (pinned) inputs uploaded every step through the public API
+    def setup_e2e(self):
+        fm = self.fm
+        self.h = []
+        for m in (self.x32, self.y32, self.x64, self.y64):
+            hb = fm.pinned(m.n_rows, 1, m.etype.value)
+            m.download_pinned(hb)
+            self.h.append(hb)
+        self.ctx.sync()
+        return sum(h.nbytes for h in self.h), 6 * 8
+
+    def step_e2e(self):
+        fm = self.fm
+        for m, hb in zip((self.x32, self.y32, self.x64, self.y64), self.h):
+            m.upload_pinned(hb)
+        if self.d.world == 1:
+            return [fm.accu(self.x32 % self.y32), fm.dot(self.x32, self.y32), fm.norm(self.x32 - self.y32),
+                    fm.accu(self.x64 % self.y64), fm.dot(self.x64, self.y64), fm.norm(self.x64 - self.y64)]
+        for f in self.launches():
+            f()
+        self.collective()
+        r = self.R.to_numpy().ravel()
+        return [r[0], r[1], float(np.sqrt(r[2])), r[3], r[4], float(np.sqrt(r[5]))]
+
+    # CPU: the reference's generated reduce kernels on a bounded sample
+    def cpu(self, n_sample: int, threads: int):
+        from oracle import fm_oracle as orc
+        data = [orc.uniform_fill(42, n_sample, "f32"), orc.uniform_fill(43, n_sample, "f32"),
+                orc.uniform_fill(42, n_sample, "f64"), orc.uniform_fill(43, n_sample, "f64")]
+        byts = 3 * (8 * n_sample + 8) + 3 * (16 * n_sample + 8)
+        try:
+            from oracle.ref_runner import RefKernels, available
+            if not available():
+                raise FileNotFoundError
+            rk = RefKernels()
+
+            def run():
+                a = rk.accu("accu_schur_f32", data[0:2], threads)
+                b = rk.accu("accu_schur_f32", data[0:2], threads)          # dot == accu(x % y)
+                c = np.sqrt(rk.accu("accu_sqdiff_f32", data[0:2], threads))
+                d = rk.accu("accu_schur_f64", data[2:4], threads)
+                e = rk.accu("accu_schur_f64", data[2:4], threads)
+                f = np.sqrt(rk.accu("accu_sqdiff_f64", data[2:4], threads))
+                return [a, b, c, d, e, f]
+            kind = "reference"
+            desc = (f"reference generated-C reduce kernels (oracle/_ref, cc -O2 -fwrapv) over "
+                    f"{n_sample:.0e}-element f32+f64 vectors, {threads} host threads on slabs")
+        except (ImportError, FileNotFoundError, OSError):
+            def run():
+                out = []
+                for x, y, et in ((data[0], data[1], orc.ElemType.f32), (data[2], data[3], orc.ElemType.f64)):
+                    p = (x * y).astype(np.float64).sum()
+                    out += [p, p, float(np.sqrt(((x - y) * (x - y)).astype(np.float64).sum()))]
+                return out
+            kind, threads = "port", 1
+            desc = f"numpy restatement (oracle/fm_oracle.py) over {n_sample:.0e}-element vectors, 1 thread"
+        return run, byts, kind, threads, desc
+
+
+# --------------------------------------------------------------------------------------
+# elementwise configs (C1, C3) and column reductions (C4): secondary bench lines
+class C1:
+    name = "c1"
+    workload = "C1 Z = 2*(X % Y) + X, f32 4096x4096"
+    unit = "GB/s"
+    dtype = "f32"
+
+    def __init__(self, args, d):
+        self.n = args.n or 4096
+        self.d = d
+        self.labels = ["c1_copy_f32"]
+        self.kbytes = [3 * 4 * self.n * self.n]
+        self.flush = True
+
+    def setup(self, fm, ctx):
+        self.fm, self.ctx = fm, ctx
+        n, off = self.n, self.d.rank * self.n * self.n
+        self.X, self.Y, self.Z = fm.Mat(n, n, "f32", ctx), fm.Mat(n, n, "f32", ctx), fm.Mat(n, n, "f32", ctx)
+        ctx.backend.randu(self.X.handle, 42, off)
+        ctx.backend.randu(self.Y.handle, 43, off)
+        self.e = 2 * (self.X % self.Y) + self.X
+        ctx.sync()
+
+    def launches(self):
+        return [lambda: self.Z.assign(self.e)]
+
+    def collective(self):
+        pass
+
+    def elements_per_step(self):
+        return self.n * self.n
+
+    def bytes_per_step(self):
+        return sum(self.kbytes)
+
+    def check(self):
+        from oracle import fm_oracle as orc
+        cols = slice(0, 8)
+        x = self.X.to_numpy()[:, cols]
+        y = self.Y.to_numpy()[:, cols]
+        want = np.float32(2) * (x * y) + x
+        return {"max_ulp_first_8_cols": orc.max_ulp(self.Z.to_numpy()[:, cols], want)}
+
+    def setup_e2e(self):
+        fm = self.fm
+        self.hx = fm.pinned(self.n, self.n, "f32")
+        self.hy = fm.pinned(self.n, self.n, "f32")
+        self.hz = fm.pinned(self.n, self.n, "f32")
+        self.X.download_pinned(self.hx)
+        self.Y.download_pinned(self.hy)
+        self.ctx.sync()
+        return self.hx.nbytes + self.hy.nbytes, self.hz.nbytes
+
+    def step_e2e(self):
+        self.X.upload_pinned(self.hx)
+        self.Y.upload_pinned(self.hy)
+        self.Z.assign(self.e)
+        self.Z.download_pinned(self.hz)
+        self.ctx.sync()
+
+    def cpu(self, n_sample, threads):
+        from oracle import fm_oracle as orc
+        n = int(np.sqrt(n_sample))
+        x = np.asfortranarray(orc.randu(n, n, 42))
+        y = np.asfortranarray(orc.randu(n, n, 43))
+        z = np.zeros((n, n), np.float32, order="F")
+        byts = 3 * 4 * n * n
+        try:
+            from oracle.ref_runner import RefKernels, available
+            if not available():
+                raise FileNotFoundError
+            rk = RefKernels()
+
+            def run():
+                rk.copy("c1_f32", z, [x, y], [np.float32(2)], threads)
+            return run, byts, "reference", threads, (
+                f"reference generated-C copy kernel (oracle/_ref) on {n}x{n}, {threads} threads on column slabs")
+        except (ImportError, FileNotFoundError, OSError):
+            def run():
+                np.add(np.float32(2) * (x * y), x, out=z)
+            return run, byts, "port", 1, f"numpy restatement on {n}x{n}, 1 thread"
+
+
+class C3(C1):
+    name = "c3"
+    workload = "C3 Z = exp(-square(X - Y)/2) + 0.5*abs(X), f32 32768x32768 per GPU (column-sharded)"
+
+    def __init__(self, args, d):
+        super().__init__(args, d)
+        self.n = args.n or 32768
+        self.kbytes = [3 * 4 * self.n * self.n]
+        self.labels = ["c3_copy_f32"]
+        self.flush = False
+
+    def setup(self, fm, ctx):
+        super().setup(fm, ctx)
+        X, Y = self.X, self.Y
+        self.e = fm.exp(-fm.square(X - Y) / 2) + 0.5 * fm.abs(X)
+
+    def check(self):
+        from oracle import fm_oracle as orc
+        cols = slice(0, 4)
+        x = self.X.to_numpy()[:, cols]
+        y = self.Y.to_numpy()[:, cols]
+        d = x - y
+        want = (np.exp((np.float32(0.5) * -(d * d)).astype(np.float64)).astype(np.float32)
+                + np.float32(0.5) * np.abs(x))
+        return {"max_ulp_first_4_cols_vs_cr": orc.max_ulp(self.Z.to_numpy()[:, cols], want)}
+
+    def cpu(self, n_sample, threads):
+        from oracle import fm_oracle as orc
+        n = int(np.sqrt(n_sample))
+        x = orc.randu(n, n, 42)
+        y = orc.randu(n, n, 43)
+        byts = 3 * 4 * n * n
+
+        def run():
+            d = x - y
+            return (np.exp((np.float32(0.5) * -(d * d)).astype(np.float64)).astype(np.float32)
+                    + np.float32(0.5) * np.abs(x))
+        return run, byts, "port", 1, f"numpy restatement (the reference has no abs) on {n}x{n}, 1 thread"
+
+
+class C4:
+    name = "c4"
+    workload = ("C4 column-wise sum/mean/max/index_max of (X - Y) % Z, f64 65536x16384 per GPU, "
+                "one fused multi-output pass (column-sharded, no exchange)")
+    unit = "GB/s"
+    dtype = "f64"
+
+    def __init__(self, args, d):
+        self.rows = 65536
+        self.cols = args.n or 16384
+        self.d = d
+        self.labels = ["c4_colstats_f64"]
+        self.kbytes = [3 * 8 * self.rows * self.cols + 3 * 8 * self.cols + 4 * self.cols]
+        self.flush = False
+
+    def setup(self, fm, ctx):
+        self.fm, self.ctx = fm, ctx
+        r, c = self.rows, self.cols
+        off = self.d.rank * r * c
+        self.X, self.Y, self.Z = (fm.Mat(r, c, "f64", ctx) for _ in range(3))
+        for m, s in ((self.X, 42), (self.Y, 43), (self.Z, 44)):
+            ctx.backend.randu(m.handle, s, off)
+        self.e = (self.X - self.Y) % self.Z
+        self.outs = [fm.Mat(1, c, "f64", ctx), fm.Mat(1, c, "f64", ctx), fm.Mat(1, c, "f64", ctx),
+                     fm.Mat(1, c, "u32", ctx)]
+        ctx.sync()
+
+    def launches(self):
+        fm, e, o = self.fm, self.e, self.outs
+        return [lambda: fm.assign_all([(o[0], fm.sum(e, 0)), (o[1], fm.mean(e, 0)),
+                                       (o[2], fm.max(e, 0)), (o[3], fm.index_max(e, 0))])]
+
+    def collective(self):
+        pass
+
+    def elements_per_step(self):
+        return self.rows * self.cols
+
+    def bytes_per_step(self):
+        return sum(self.kbytes)
+
+    def check(self):
+        from oracle import fm_oracle as orc
+        cols = slice(0, 16)
+        v = (self.X.to_numpy()[:, cols] - self.Y.to_numpy()[:, cols]) * self.Z.to_numpy()[:, cols]
+        k = orc.ReduceKind
+        return {"index_max_exact_16_cols": bool(np.array_equal(
+                    self.outs[3].to_numpy()[:, cols], orc.reduce_dim(k.index_max, 0, v, orc.ElemType.f64))),
+                "sum_rel_err_16_cols": orc.compare(self.outs[0].to_numpy()[:, cols],
+                                                   orc.reduce_dim(k.sum, 0, v, orc.ElemType.f64))}
+
+    def setup_e2e(self):
+        return None
+
+    def cpu(self, n_sample, threads):
+        from oracle import fm_oracle as orc
+        cols = max(1, n_sample // self.rows)
+        X = orc.randu(self.rows, cols, 42, "f64")
+        Y = orc.randu(self.rows, cols, 43, "f64")
+        Z = orc.randu(self.rows, cols, 44, "f64")
+        byts = 3 * 8 * self.rows * cols
+
+        def run():
+            v = (X - Y) * Z
+            k = orc.ReduceKind
+            return [orc.reduce_dim(kk, 0, v, orc.ElemType.f64) for kk in (k.sum, k.mean, k.max, k.index_max)]
+        return run, byts, "port", 1, f"numpy restatement on {self.rows}x{cols}, 1 thread"
+
+
+CONFIGS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4}
+
+
+# --------------------------------------------------------------------------------------
+def time_cpu(run, byts, steps, warmup):
+    for _ in range(warmup):
+        run()
+    t = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        run()
+        t.append(time.perf_counter() - t0)
+    return byts / statistics.fmean(t) / 1e9, statistics.fmean(t)
+
+
+def cpu_sample_elems(cfg_name: str) -> int:
+    return {"c2": 20_000_000, "c1": 4096 * 4096, "c3": 4096 * 4096, "c4": 65536 * 64}[cfg_name]
+
+
+def reference_arm(args, d: Dist):
+    if d.rank != 0:
+        return 0
+    cfg = CONFIGS[args.config](args, d)
+    threads = os.cpu_count() or 1
+    run, byts, kind, threads, desc = cfg.cpu(cpu_sample_elems(args.config), threads)
+    steps = max(1, args.steps)
+    gbs, mean_s = time_cpu(run, byts, steps, max(1, args.warmup))
+    line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": cfg.unit,
+            "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": round(mean_s * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (reference splitmix64 randu)",
+            "config": {"workload": cfg.workload, "sample": desc},
+            "cpu_baseline": {"value": round(gbs, 3), "unit": cfg.unit, "cores": threads, "kind": kind,
+                             "sample": desc},
+            "e2e": {"value": round(gbs, 3), "unit": cfg.unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def ours(args, d: Dist):
+    import paper_2604_22242_b200 as fm
+    from paper_2604_22242_b200._native import native
+
+    nat = native()
+    backend = fm.B200Backend(device=d.local)
+    ctx = fm.Context(backend)
+    cfg = CONFIGS[args.config](args, d)
+    cfg.setup(fm, ctx)
+    launches = cfg.launches()
+    nk = len(launches)
+    ev = Events(nat, backend.stream, (nk + 1) * args.steps + 2)
+    flush_h = None
+    if getattr(cfg, "flush", False):
+        flush_h = backend.alloc(fm.ElemType.f32, 256 * 1024 * 1024 // 4 * 2)   # 512 MiB > 126 MB L2
+
+    # warm-up: kernels, caches, plans
+    for _ in range(args.warmup):
+        for f in launches:
+            f()
+        cfg.collective()
+    ctx.sync()
+    d.barrier()
+
+    sampler = ClockSampler(d.local)
+    sampler.start()
+    time.sleep(0.3)
+    ctx.sync()
+    d.barrier()
+    c0 = nat.lib.fm_launch_counter()
+    per_kernel = [[] for _ in range(nk)]
+    steps_ms = []
+    t_wall0 = time.perf_counter()
+    for s in range(args.steps):
+        if flush_h is not None:
+            nat.call("fm_flush_l2", backend.ptr(flush_h), flush_h.n_elem * 4, backend.stream)
+        base = s * (nk + 1)
+        ev.record(base)
+        for i, f in enumerate(launches):
+            f()
+            ev.record(base + i + 1)
+        cfg.collective()
+        if d.world > 1:
+            ev.record(base + nk)   # collective lands in the last kernel's slot end
+    ctx.sync()
+    d.barrier()
+    t_wall = time.perf_counter() - t_wall0
+    c1 = nat.lib.fm_launch_counter()
+    clocks = sampler.stop()
+    for s in range(args.steps):
+        base = s * (nk + 1)
+        for i in range(nk):
+            per_kernel[i].append(ev.ms(base + i, base + i + 1))
+        steps_ms.append(ev.ms(base, base + nk))
+    total_ms = sum(steps_ms)
+    total_ms = d.max(total_ms)
+    ms_per_step = total_ms / args.steps
+    bytes_all = cfg.bytes_per_step() * d.world
+    value = bytes_all / (ms_per_step * 1e-3) / 1e9
+    peaks = measured_peaks()
+    # dominant kernel: largest share of device time
+    means = [statistics.fmean(v) for v in per_kernel]
+    share = [sum(v) for v in per_kernel]
+    dom = int(np.argmax(share))
+    achieved = cfg.kbytes[dom] / (means[dom] * 1e-3) / 1e9
+    traffic = ncu_traffic(cfg.labels[dom])
+    roofline = {"bound": "hbm", "kernel": cfg.labels[dom], "achieved": round(achieved, 1),
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                "frac_of_8TBs": round(achieved / SPEC_HBM_GBS, 4),
+                "peak_source": peaks["source"], "traffic": traffic,
+                "algorithmic_bytes_per_launch": cfg.kbytes[dom],
+                "mean_launch_us": round(means[dom] * 1e3, 2),
+                "per_kernel_gbs": {lab: round(b / (m * 1e-3) / 1e9, 1)
+                                   for lab, b, m in zip(cfg.labels, cfg.kbytes, means)}}
+    check = cfg.check()
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        io = cfg.setup_e2e()
+        if io is not None:
+            h2d, d2h = io
+            cfg.step_e2e()
+            ctx.sync()
+            d.barrier()
+            t = []
+            for _ in range(max(2, min(args.steps, 5))):
+                ctx.sync()
+                d.barrier()
+                t0 = time.perf_counter()
+                cfg.step_e2e()
+                ctx.sync()
+                t.append(time.perf_counter() - t0)
+            e2e_s = d.max(statistics.fmean(t))
+            e2e = {"value": round(bytes_all / e2e_s / 1e9, 3), "unit": cfg.unit,
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                   "ms_per_step": round(e2e_s * 1e3, 3),
+                   "path": "public API: Mat.upload_pinned + fm.accu/dot/norm (host floats back)"
+                   if cfg.name == "c2" else "public API: upload_pinned + Mat.assign + download_pinned"}
+
+    # CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if d.world == 1 and not args.no_cpu:
+        run, byts, kind, threads, desc = cfg.cpu(cpu_sample_elems(cfg.name), os.cpu_count() or 1)
+        gbs, _ = time_cpu(run, byts, 3, 1)
+        cpu = {"value": round(gbs, 3), "unit": cfg.unit, "cores": threads, "kind": kind, "sample": desc}
+
+    if d.rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": cfg.unit, "n_gpus": d.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": cfg.dtype, "data": "synthetic (reference splitmix64 randu, generated on device)",
+            "config": {"workload": cfg.workload,
+                       "elements_per_gpu_per_step": cfg.elements_per_step(),
+                       "algorithmic_bytes_per_gpu_per_step": cfg.bytes_per_step(),
+                       "l2": ("L2 flushed (512 MiB write) before every timed step" if flush_h is not None
+                              else "inputs larger than the 126 MB L2; no flush"),
+                       "parallelism": f"column/slice sharded x{d.world}, one process per GPU"
+                                      + (", one NCCL all_reduce of partials per step" if cfg.name == "c2" and d.world > 1 else "")},
+            "elements_per_s": round(cfg.elements_per_step() * d.world / (ms_per_step * 1e-3), 1),
+            "pct_of_8TBs": round(100 * value / d.world / SPEC_HBM_GBS, 2),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(c1 - c0), "clocks": clocks,
+            "wall_s_timed_region": round(t_wall, 4), "check": check,
+        }
+        print(json.dumps(line, default=float), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--n", type=int, default=0, help="override the per-GPU size")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    d = Dist() if args.impl == "ours" or int(os.environ.get("WORLD_SIZE", "1")) > 1 else Dist()
+    try:
+        if args.impl == "reference":
+            return reference_arm(args, d)
+        return ours(args, d)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,88 @@
+// launch.cuh -- host-side launchers of the skeletons for one evaluator type.
+// Grid sizing follows the B200 measurements in profiles/: memory-bound
+// grid-stride kernels want many resident warps and several waves, so grids
+// are multiples of the SM count (148) capped where partial results must be
+// combined.
+#pragma once
+#include "common.cuh"
+#include "skeletons.cuh"
+
+namespace fm {
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+template <class E>
+int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s) {
+  constexpr int V = E::kV;
+  if (n_rows == 0 || n_cols == 0) return 0;
+  const int64_t nrb = cdiv(n_rows, V);
+  const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;
+  const int64_t grid = std::min<int64_t>(cdiv(nch, kThreads), (int64_t)sm_count() * 32);
+  k_copy<E><<<(unsigned)grid, kThreads, 0, s>>>(P, out, n_rows, n_cols);
+  FM_CHECK_LAUNCH("fused copy kernel");
+  return 0;
+}
+
+template <class E>
+int run_accu(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, int finalize,
+             cudaStream_t s) {
+  constexpr int V = E::kV;
+  const int64_t nrb = cdiv(n_rows, V);
+  const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(cdiv(nch, kThreads), (int64_t)sm_count() * 8));
+  Scratch sc;
+  int st = get_scratch((void *)s, grid * (sizeof(double) + sizeof(uint32_t)) + 64, &sc);
+  if (st) return st;
+  double *pd = (double *)sc.payload;
+  uint32_t *pu = (uint32_t *)(pd + grid);
+  k_accu<E><<<(unsigned)grid, kThreads, 0, s>>>(P, out, n_rows, n_cols, finalize, pd, pu, sc.counters);
+  FM_CHECK_LAUNCH("fused accu kernel");
+  return 0;
+}
+
+template <class E>
+int run_reduce_dim(const fm_program &P, int dim, int64_t n_rows, int64_t n_cols, const ReduceOuts &R,
+                   cudaStream_t s) {
+  constexpr int V = E::kV;
+  if (n_rows == 0 || n_cols == 0) {
+    return 0;
+  }
+  if (dim == 0) {
+    const int64_t grid = std::min<int64_t>(n_cols, (int64_t)sm_count() * 8);
+    k_reduce_cols<E><<<(unsigned)grid, kThreads, 0, s>>>(P, R, n_rows, n_cols);
+    FM_CHECK_LAUNCH("fused column-reduction kernel");
+    return 0;
+  }
+  const int64_t gx = cdiv(n_rows, (int64_t)kThreads * V);
+  if (gx > 65535 * 1024LL) return fail_msg("reduce_dim: too many rows");
+  int64_t splits = std::max<int64_t>(1, cdiv((int64_t)sm_count() * 4, gx));
+  splits = std::min<int64_t>(splits, std::min<int64_t>(n_cols, 65535));
+  RowPartial *part = nullptr;
+  unsigned *counters = nullptr;
+  if (splits > 1) {
+    Scratch sc;
+    int st = get_scratch((void *)s, (size_t)(splits * n_rows) * sizeof(RowPartial), &sc);
+    if (st) return st;
+    if ((size_t)gx * sizeof(unsigned) > 64 * 1024) return fail_msg("reduce_dim: counter space exhausted");
+    part = (RowPartial *)sc.payload;
+    counters = sc.counters;
+  }
+  dim3 grid((unsigned)gx, (unsigned)splits);
+  k_reduce_rows<E><<<grid, kThreads, 0, s>>>(P, R, n_rows, n_cols, part, counters);
+  FM_CHECK_LAUNCH("fused row-reduction kernel");
+  return 0;
+}
+
+// Registry of ahead-of-time template kernels (templates.cu, generated).
+enum { SK_COPY = 0, SK_ACCU = 1, SK_DIM0 = 2, SK_DIM1 = 3 };
+struct TemplateEntry {
+  const char *signature;   // bare expression signature (exprtree.signature_of)
+  int (*copy)(const fm_program &, void *, int64_t, int64_t, cudaStream_t);
+  int (*accu)(const fm_program &, void *, int64_t, int64_t, int, cudaStream_t);
+  int (*reduce_dim)(const fm_program &, int, int64_t, int64_t, const ReduceOuts &, cudaStream_t);
+  int n_inputs;
+  int etype;
+};
+const TemplateEntry *template_table(int *n);
+
+}  // namespace fm

@@ -1,0 +1,199 @@
+// runtime.cu -- device, memory, stream, event entry points of the C ABI and
+// the shared scratch / error plumbing (include/fmb200.h).
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace fm {
+
+static thread_local std::string g_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string &msg) { g_error = msg; }
+int fail(const char *what, cudaError_t e) {
+  set_error(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+  return (int)e == 0 ? -1 : (int)e;
+}
+int fail_msg(const std::string &msg) {
+  set_error(msg);
+  return -1;
+}
+void count_launch(int64_t n) { g_launches += n; }
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && cached[dev]) return cached[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev < 64) cached[dev] = n;
+  return n;
+}
+
+static constexpr size_t kCounterBytes = 64 * 1024;
+struct ScratchEntry {
+  void *base = nullptr;
+  size_t payload = 0;
+};
+static std::mutex g_scratch_mu;
+static std::map<std::pair<int, void *>, ScratchEntry> g_scratch;
+
+int get_scratch(void *stream, size_t payload_bytes, Scratch *out) {
+  int dev = 0;
+  FM_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  ScratchEntry &e = g_scratch[{dev, stream}];
+  cudaStream_t s = (cudaStream_t)stream;
+  if (e.base == nullptr || e.payload < payload_bytes) {
+    size_t want = payload_bytes < (size_t)(1 << 20) ? (size_t)(1 << 20) : payload_bytes;
+    if (e.base) FM_CHECK(cudaFreeAsync(e.base, s));
+    FM_CHECK(cudaMallocAsync(&e.base, kCounterBytes + want, s));
+    FM_CHECK(cudaMemsetAsync(e.base, 0, kCounterBytes, s));
+    e.payload = want;
+  }
+  out->counters = (unsigned *)e.base;
+  out->payload = (char *)e.base + kCounterBytes;
+  out->payload_bytes = e.payload;
+  return 0;
+}
+
+}  // namespace fm
+
+using namespace fm;
+
+extern "C" {
+
+const char *fm_last_error(void) { return g_error.c_str(); }
+int fm_abi_version(void) { return FMB200_ABI_VERSION; }
+int64_t fm_launch_counter(void) { return g_launches.load(); }
+
+int fm_device_count(int *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    cudaGetLastError();
+    return fail("cudaGetDeviceCount", e);
+  }
+  *count = n;
+  return 0;
+}
+
+int fm_set_device(int device) {
+  FM_CHECK(cudaSetDevice(device));
+  return 0;
+}
+
+int fm_get_device(int *device) {
+  FM_CHECK(cudaGetDevice(device));
+  return 0;
+}
+
+int fm_device_info(int device, int *sm, int *major, int *minor, int64_t *l2, int64_t *hbm) {
+  cudaDeviceProp p;
+  FM_CHECK(cudaGetDeviceProperties(&p, device));
+  *sm = p.multiProcessorCount;
+  *major = p.major;
+  *minor = p.minor;
+  *l2 = p.l2CacheSize;
+  *hbm = (int64_t)p.totalGlobalMem;
+  return 0;
+}
+
+int fm_alloc(void **ptr, size_t bytes, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (bytes == 0) bytes = 1;
+  FM_CHECK(cudaMallocAsync(ptr, bytes, s));
+  FM_CHECK(cudaMemsetAsync(*ptr, 0, bytes, s));
+  return 0;
+}
+
+int fm_free(void *ptr, void *stream) {
+  if (!ptr) return 0;
+  FM_CHECK(cudaFreeAsync(ptr, (cudaStream_t)stream));
+  return 0;
+}
+
+int fm_host_alloc(void **ptr, size_t bytes) {
+  FM_CHECK(cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocPortable));
+  return 0;
+}
+
+int fm_host_free(void *ptr) {
+  FM_CHECK(cudaFreeHost(ptr));
+  return 0;
+}
+
+int fm_memcpy_h2d(void *dst, const void *src, size_t bytes, void *stream) {
+  FM_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return 0;
+}
+
+int fm_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream) {
+  FM_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  return 0;
+}
+
+int fm_memcpy_d2d(void *dst, const void *src, size_t bytes, void *stream) {
+  FM_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return 0;
+}
+
+int fm_memset(void *dst, int value, size_t bytes, void *stream) {
+  FM_CHECK(cudaMemsetAsync(dst, value, bytes, (cudaStream_t)stream));
+  return 0;
+}
+
+int fm_stream_create(void **stream) {
+  cudaStream_t s;
+  FM_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  // keep freed blocks in the pool: cudaMallocAsync then costs ~1 us
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *stream = (void *)s;
+  return 0;
+}
+
+int fm_stream_destroy(void *stream) {
+  FM_CHECK(cudaStreamDestroy((cudaStream_t)stream));
+  return 0;
+}
+
+int fm_stream_sync(void *stream) {
+  FM_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+  return 0;
+}
+
+int fm_event_create(void **event) {
+  cudaEvent_t e;
+  FM_CHECK(cudaEventCreate(&e));
+  *event = (void *)e;
+  return 0;
+}
+
+int fm_event_destroy(void *event) {
+  FM_CHECK(cudaEventDestroy((cudaEvent_t)event));
+  return 0;
+}
+
+int fm_event_record(void *event, void *stream) {
+  FM_CHECK(cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream));
+  return 0;
+}
+
+int fm_event_elapsed_ms(void *start, void *stop, float *ms) {
+  FM_CHECK(cudaEventSynchronize((cudaEvent_t)stop));
+  FM_CHECK(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)stop));
+  return 0;
+}
+
+}  // extern "C"

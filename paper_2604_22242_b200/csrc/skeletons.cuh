@@ -1,0 +1,473 @@
+// skeletons.cuh -- the three launch skeletons, templated on an evaluator.
+//
+//   copy       : out[r + c*n_rows] = EXPR(r, c)          (codegen.py:74-92)
+//   accu       : *out = sum EXPR, f64 / wrapping int     (codegen.py:94-114)
+//   reduce_dim : sum / mean / max / min / index_max / index_min of EXPR per
+//                column (dim 0) or per row (dim 1), several outputs per pass
+//
+// An evaluator E provides kV (elements per thread) and
+//   static void eval(const fm_program&, const Chunk&, uint32_t (&lo)[kV], uint32_t (&hi)[kV])
+// returning the result bits of V consecutive elements (the root's element
+// type is P.result_etype).
+#pragma once
+#include "vm.cuh"
+
+namespace fm {
+
+constexpr int kThreads = 256;
+
+struct ReduceOuts {
+  fm_reduce_out o[FM_MAX_REDUCE_OUT];
+  int n;
+};
+
+// ---- typed helpers -----------------------------------------------------------------
+FM_DEV bool is_float_etype(int e) { return e == FM_F32 || e == FM_F64 || e == FM_BF16; }
+
+// value of element v as f64 (exact for every element type)
+FM_DEV double as_double(int etype, uint32_t lo, uint32_t hi) {
+  switch (etype) {
+    case FM_F64: return u2d(lo, hi);
+    case FM_U32: return (double)lo;
+    case FM_I32: return (double)(int32_t)lo;
+    default: return (double)u2f(lo);   // f32 and bf16 (held as f32)
+  }
+}
+
+FM_DEV void st_v4(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+template <int V>
+FM_DEV void store_chunk(void *out, int etype, int64_t base, int cnt, const uint32_t (&lo)[V],
+                        const uint32_t (&hi)[V]) {
+  if (etype == FM_F64) {
+    unsigned long long *p = (unsigned long long *)out + base;
+    if (cnt == V && (((uintptr_t)p) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < V / 2; ++q) st_v4(p + 2 * q, lo[2 * q], hi[2 * q], lo[2 * q + 1], hi[2 * q + 1]);
+      return;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (v < cnt) p[v] = ((unsigned long long)hi[v] << 32) | lo[v];
+  } else if (etype == FM_BF16) {
+    uint16_t *p = (uint16_t *)out + base;
+    if (V == 8 && cnt == V && (((uintptr_t)p) & 15) == 0) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = (lo[(2 * q) % V] >> 16) | (lo[(2 * q + 1) % V] & 0xffff0000u);
+      st_v4(p, w[0], w[1], w[2], w[3]);
+      return;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (v < cnt) p[v] = (uint16_t)(lo[v] >> 16);
+  } else {
+    uint32_t *p = (uint32_t *)out + base;
+    if (cnt == V && (((uintptr_t)p) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < V / 4; ++q) st_v4(p + 4 * q, lo[4 * q], lo[4 * q + 1], lo[4 * q + 2], lo[4 * q + 3]);
+      return;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (v < cnt) p[v] = lo[v];
+  }
+}
+
+// Chunk number c of the domain.  Flat programs chunk the flat index space;
+// others chunk each column into runs of V rows.
+template <int V>
+FM_DEV Chunk make_chunk(const fm_program &P, int64_t c, int64_t n_rows, int64_t n_elem, int64_t nrb) {
+  Chunk ch;
+  if (P.flat) {
+    ch.base = c * V;
+    ch.cnt = (int)min((int64_t)V, n_elem - ch.base);
+    ch.row0 = 0; ch.col = 0; ch.flat = true;
+  } else {
+    ch.col = c / nrb;
+    ch.row0 = (c - ch.col * nrb) * V;
+    ch.cnt = (int)min((int64_t)V, n_rows - ch.row0);
+    ch.base = ch.row0 + ch.col * n_rows;
+    ch.flat = false;
+  }
+  return ch;
+}
+
+template <int V>
+FM_DEV int64_t chunk_count(const fm_program &P, int64_t n_rows, int64_t n_cols, int64_t &nrb) {
+  nrb = (n_rows + V - 1) / V;
+  return P.flat ? (n_rows * n_cols + V - 1) / V : nrb * n_cols;
+}
+
+// ---- copy ------------------------------------------------------------------------------
+template <class E>
+__global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ fm_program P, void *out,
+                                                   int64_t n_rows, int64_t n_cols) {
+  constexpr int V = E::kV;
+  int64_t nrb;
+  const int64_t nch = chunk_count<V>(P, n_rows, n_cols, nrb);
+  const int64_t n_elem = n_rows * n_cols;
+  for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < nch; c += (int64_t)gridDim.x * kThreads) {
+    Chunk ch = make_chunk<V>(P, c, n_rows, n_elem, nrb);
+    uint32_t lo[V], hi[V];
+    E::eval(P, ch, lo, hi);
+    store_chunk<V>(out, P.result_etype, ch.base, ch.cnt, lo, hi);
+  }
+}
+
+// ---- block reductions ------------------------------------------------------------------------
+FM_DEV double warp_sum_d(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+FM_DEV uint32_t warp_sum_u(uint32_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// (value, index) candidate for max / min with numpy semantics: NaN wins
+// (first NaN), ties keep the lowest index.
+struct Cand {
+  double v;
+  int64_t i;
+};
+FM_DEV bool better_max(const Cand &a, const Cand &b) {
+  const bool an = a.v != a.v, bn = b.v != b.v;
+  if (an || bn) return an && (!bn || a.i < b.i);
+  return a.v > b.v || (a.v == b.v && a.i < b.i);
+}
+FM_DEV bool better_min(const Cand &a, const Cand &b) {
+  const bool an = a.v != a.v, bn = b.v != b.v;
+  if (an || bn) return an && (!bn || a.i < b.i);
+  return a.v < b.v || (a.v == b.v && a.i < b.i);
+}
+FM_DEV Cand shfl_cand(const Cand &c, int o) {
+  Cand r;
+  r.v = __shfl_xor_sync(0xffffffffu, c.v, o);
+  r.i = __shfl_xor_sync(0xffffffffu, c.i, o);
+  return r;
+}
+template <bool MAX>
+FM_DEV Cand warp_best(Cand c) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Cand x = shfl_cand(c, o);
+    if (MAX ? better_max(x, c) : better_min(x, c)) c = x;
+  }
+  return c;
+}
+
+// block-wide helpers (kThreads threads; result valid in thread 0)
+FM_DEV double block_sum_d(double x, double *sm) {
+  x = warp_sum_d(x);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm[w] = x;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = (l < kThreads / 32) ? sm[l] : 0.0;
+    r = warp_sum_d(r);
+  }
+  return r;
+}
+FM_DEV uint32_t block_sum_u(uint32_t x, uint32_t *sm) {
+  x = warp_sum_u(x);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm[w] = x;
+  __syncthreads();
+  uint32_t r = 0;
+  if (threadIdx.x < 32) {
+    r = (l < kThreads / 32) ? sm[l] : 0u;
+    r = warp_sum_u(r);
+  }
+  return r;
+}
+template <bool MAX>
+FM_DEV Cand block_best(Cand c, Cand *sm) {
+  c = warp_best<MAX>(c);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm[w] = c;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    c = (l < kThreads / 32) ? sm[l] : sm[0];
+    c = warp_best<MAX>(c);
+  }
+  return c;
+}
+
+// ---- accu ------------------------------------------------------------------------------------
+// Per-block partials then a last-block finish: ONE launch, deterministic for
+// a given grid (fixed per-thread order, fixed tree).
+template <class E>
+__global__ void __launch_bounds__(kThreads) k_accu(const __grid_constant__ fm_program P, void *out,
+                                                   int64_t n_rows, int64_t n_cols, int finalize,
+                                                   double *part_d, uint32_t *part_u, unsigned *counter) {
+  constexpr int V = E::kV;
+  __shared__ double smd[kThreads / 32];
+  __shared__ uint32_t smu[kThreads / 32];
+  __shared__ bool last;
+  const int rt = P.result_etype;
+  const bool fl = is_float_etype(rt);
+  int64_t nrb;
+  const int64_t nch = chunk_count<V>(P, n_rows, n_cols, nrb);
+  const int64_t n_elem = n_rows * n_cols;
+  double accd = 0.0;
+  uint32_t accu = 0;
+  for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < nch; c += (int64_t)gridDim.x * kThreads) {
+    Chunk ch = make_chunk<V>(P, c, n_rows, n_elem, nrb);
+    uint32_t lo[V], hi[V];
+    E::eval(P, ch, lo, hi);
+    if (fl) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (v < ch.cnt) accd += as_double(rt, lo[v], hi[v]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (v < ch.cnt) accu += lo[v];
+    }
+  }
+  double bd = block_sum_d(accd, smd);
+  uint32_t bu = block_sum_u(accu, smu);
+  if (threadIdx.x == 0) {
+    part_d[blockIdx.x] = bd;
+    part_u[blockIdx.x] = bu;
+    __threadfence();
+    unsigned t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double sd = 0.0;
+  uint32_t su = 0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += kThreads) {
+    sd += ((volatile double *)part_d)[i];
+    su += ((volatile uint32_t *)part_u)[i];
+  }
+  sd = block_sum_d(sd, smd);
+  su = block_sum_u(su, smu);
+  if (threadIdx.x == 0) {
+    if (fl) {
+      if (finalize == FM_FINAL_SQRT) sd = sqrt_d(sd);
+      *(double *)out = sd;
+    } else {
+      *(uint32_t *)out = su;
+    }
+    *counter = 0u;   // self-reset for the next launch on this stream
+  }
+}
+
+// ---- reduce_dim ------------------------------------------------------------------------------------
+struct Stats {
+  double sum;
+  uint32_t usum;
+  Cand mx, mn;
+};
+
+FM_DEV void stats_init(Stats &s) {
+  s.sum = 0.0; s.usum = 0;
+  s.mx.v = __longlong_as_double(0xfff0000000000000ll); s.mx.i = INT64_MAX;   // -inf
+  s.mn.v = __longlong_as_double(0x7ff0000000000000ll); s.mn.i = INT64_MAX;   // +inf
+}
+
+FM_DEV void stats_add(Stats &s, int rt, bool fl, uint32_t lo, uint32_t hi, int64_t idx, unsigned need) {
+  if (fl || !(need & 1u)) {
+    const double x = as_double(rt, lo, hi);
+    if (need & 1u) s.sum += x;
+    Cand c{x, idx};
+    if ((need & 2u) && better_max(c, s.mx)) s.mx = c;
+    if ((need & 4u) && better_min(c, s.mn)) s.mn = c;
+  } else {
+    s.usum += lo;
+    const double x = as_double(rt, lo, hi);
+    Cand c{x, idx};
+    if ((need & 2u) && better_max(c, s.mx)) s.mx = c;
+    if ((need & 4u) && better_min(c, s.mn)) s.mn = c;
+  }
+}
+
+// write one reduced value of kind k at position pos
+FM_DEV void emit_out(const fm_reduce_out &o, int64_t pos, const Stats &s, int rt, bool fl, int64_t n_along) {
+  switch (o.kind) {
+    case FM_RED_SUM:
+    case FM_RED_MEAN: {
+      if (!fl) {   // integer sum wraps in the element type
+        ((uint32_t *)o.out)[pos] = s.usum;
+        return;
+      }
+      double v = s.sum;
+      if (o.kind == FM_RED_MEAN) v = div_d(v, (double)n_along);
+      if (o.etype == FM_F64) ((double *)o.out)[pos] = v;
+      else if (o.etype == FM_BF16) ((uint16_t *)o.out)[pos] = (uint16_t)(f2u(d_to_bf(v)) >> 16);
+      else ((float *)o.out)[pos] = d_to_f(v);
+      return;
+    }
+    case FM_RED_MAX:
+    case FM_RED_MIN: {
+      const double v = (o.kind == FM_RED_MAX) ? s.mx.v : s.mn.v;
+      switch (o.etype) {
+        case FM_F64: ((double *)o.out)[pos] = v; break;
+        case FM_F32: ((float *)o.out)[pos] = (float)v; break;
+        case FM_BF16: ((uint16_t *)o.out)[pos] = (uint16_t)(f2u((float)v) >> 16); break;
+        case FM_U32: ((uint32_t *)o.out)[pos] = (uint32_t)v; break;
+        default: ((int32_t *)o.out)[pos] = (int32_t)v; break;
+      }
+      return;
+    }
+    case FM_RED_IMAX: ((uint32_t *)o.out)[pos] = (uint32_t)s.mx.i; return;
+    default: ((uint32_t *)o.out)[pos] = (uint32_t)s.mn.i; return;
+  }
+}
+
+FM_DEV unsigned needed_stats(const ReduceOuts &R) {
+  unsigned need = 0;
+  for (int i = 0; i < R.n; ++i) {
+    const int k = R.o[i].kind;
+    if (k == FM_RED_SUM || k == FM_RED_MEAN) need |= 1u;
+    else if (k == FM_RED_MAX || k == FM_RED_IMAX) need |= 2u;
+    else need |= 4u;
+  }
+  return need;
+}
+
+// dim 0: one block per column (grid-stride over columns)
+template <class E>
+__global__ void __launch_bounds__(kThreads) k_reduce_cols(const __grid_constant__ fm_program P,
+                                                          const __grid_constant__ ReduceOuts R,
+                                                          int64_t n_rows, int64_t n_cols) {
+  constexpr int V = E::kV;
+  __shared__ double smd[kThreads / 32];
+  __shared__ uint32_t smu[kThreads / 32];
+  __shared__ Cand smc[kThreads / 32];
+  const int rt = P.result_etype;
+  const bool fl = is_float_etype(rt);
+  const unsigned need = needed_stats(R);
+  for (int64_t col = blockIdx.x; col < n_cols; col += gridDim.x) {
+    Stats s;
+    stats_init(s);
+    for (int64_t row0 = (int64_t)threadIdx.x * V; row0 < n_rows; row0 += (int64_t)kThreads * V) {
+      Chunk ch;
+      ch.row0 = row0; ch.col = col; ch.base = row0 + col * n_rows;
+      ch.cnt = (int)min((int64_t)V, n_rows - row0);
+      ch.flat = P.flat != 0;
+      uint32_t lo[V], hi[V];
+      E::eval(P, ch, lo, hi);
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (v < ch.cnt) stats_add(s, rt, fl, lo[v], hi[v], row0 + v, need);
+    }
+    Stats t = s;
+    if (need & 1u) {
+      t.sum = block_sum_d(s.sum, smd);
+      t.usum = block_sum_u(s.usum, smu);
+    }
+    if (need & 2u) t.mx = block_best<true>(s.mx, smc);
+    if (need & 4u) t.mn = block_best<false>(s.mn, smc);
+    if (threadIdx.x == 0)
+      for (int i = 0; i < R.n; ++i) emit_out(R.o[i], col, t, rt, fl, n_rows);
+    __syncthreads();
+  }
+}
+
+// dim 1: each thread owns V consecutive rows; blockIdx.y splits the columns.
+// With several splits, partial stats go to scratch and the last block of each
+// row tile combines them in split order (one launch, deterministic).
+struct RowPartial {
+  double sum;
+  uint32_t usum;
+  uint32_t pad;
+  Cand mx, mn;
+};
+
+template <class E>
+__global__ void __launch_bounds__(kThreads) k_reduce_rows(const __grid_constant__ fm_program P,
+                                                          const __grid_constant__ ReduceOuts R,
+                                                          int64_t n_rows, int64_t n_cols,
+                                                          RowPartial *part, unsigned *counters) {
+  constexpr int V = E::kV;
+  __shared__ bool last;
+  const int rt = P.result_etype;
+  const bool fl = is_float_etype(rt);
+  const unsigned need = needed_stats(R);
+  const int splits = gridDim.y;
+  const int64_t cols_per = (n_cols + splits - 1) / splits;
+  const int64_t c0 = (int64_t)blockIdx.y * cols_per;
+  const int64_t c1 = min(n_cols, c0 + cols_per);
+  const int64_t row0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * V;
+  const bool active = row0 < n_rows;
+  const int cnt = active ? (int)min((int64_t)V, n_rows - row0) : 0;
+  Stats s[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) stats_init(s[v]);
+  if (active) {
+    for (int64_t col = c0; col < c1; ++col) {
+      Chunk ch;
+      ch.row0 = row0; ch.col = col; ch.base = row0 + col * n_rows; ch.cnt = cnt;
+      ch.flat = P.flat != 0;
+      uint32_t lo[V], hi[V];
+      E::eval(P, ch, lo, hi);
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (v < cnt) stats_add(s[v], rt, fl, lo[v], hi[v], col, need);
+    }
+  }
+  if (splits == 1) {
+    if (active)
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (v < cnt)
+          for (int i = 0; i < R.n; ++i) emit_out(R.o[i], row0 + v, s[v], rt, fl, n_cols);
+    return;
+  }
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (v < cnt) {
+        RowPartial p;
+        p.sum = s[v].sum; p.usum = s[v].usum; p.pad = 0; p.mx = s[v].mx; p.mn = s[v].mn;
+        part[(int64_t)blockIdx.y * n_rows + row0 + v] = p;
+      }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = atomicAdd(&counters[blockIdx.x], 1u);
+    last = (t == (unsigned)splits - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (v >= cnt) continue;
+      Stats t;
+      stats_init(t);
+      for (int y = 0; y < splits; ++y) {
+        const RowPartial *pp = &part[(int64_t)y * n_rows + row0 + v];
+        const double ps = ((volatile const double *)&pp->sum)[0];
+        const uint32_t pu = ((volatile const uint32_t *)&pp->usum)[0];
+        Cand pmx, pmn;
+        pmx.v = ((volatile const double *)&pp->mx.v)[0];
+        pmx.i = ((volatile const int64_t *)&pp->mx.i)[0];
+        pmn.v = ((volatile const double *)&pp->mn.v)[0];
+        pmn.i = ((volatile const int64_t *)&pp->mn.i)[0];
+        t.sum += ps; t.usum += pu;
+        if (better_max(pmx, t.mx)) t.mx = pmx;
+        if (better_min(pmn, t.mn)) t.mn = pmn;
+      }
+      for (int i = 0; i < R.n; ++i) emit_out(R.o[i], row0 + v, t, rt, fl, n_cols);
+    }
+  }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
+}
+
+}  // namespace fm

@@ -1,0 +1,328 @@
+"""Execution planning: fused launches, folded GEMMs and reduction roots.
+
+Follows the reference planner (`/root/reference/pkg/src/fusemat/plan.py:113-215`):
+every maximal MatMul-free subtree becomes exactly one fused launch, real
+matrices keep their non-negative ids, temporaries get fresh negative ids and an
+unsafe alias lands in a temp the caller swaps in.  B200-specific changes:
+
+* `MatMul(s * A, B.t())`-style operands are folded into ONE `GemmStep`: scalar
+  pre-multiplies become `alpha` and transposes become operand major-ness
+  (the reference emits two copy kernels plus a GEMM, `plan.py:125-151`).
+  Only operands that are not (scaled, transposed) dense leaves are
+  materialised.
+* `Reduce` roots plan to a single `FusedKernelStep` with a dim-reduction
+  skeleton; several reductions of the same subexpression can share one launch
+  (`plan_many`).
+* `reduce_plan` (accu) is unchanged: a 1x1 accumulator temp of
+  `accumulator_type` (`plan.py:208-215`).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .errors import PlanError
+from .exprtree import (
+    AliasKind, BinaryElem, Diag, ElemType, ExprNode, InputSpec, Leaf, MatMul,
+    MatShape, Reduce, ReduceKind, ScalarSlot, Subview, Transpose, UnaryElem,
+    UnaryKind, aliases, collect_inputs, signature_of,
+)
+
+COPY = "copy"
+REDUCE_ACCU = "reduce_accu"
+REDUCE_DIM = "reduce_dim"
+
+# accu finalisers (applied once to the f64 total inside the last block)
+FINAL_NONE = 0
+FINAL_SQRT = 1
+
+
+def accumulator_type(etype: ElemType) -> ElemType:
+    """f64 for floats, modular native type for ints (`codegen.py:47-49`)."""
+    return ElemType.f64 if etype.is_float else etype
+
+
+def qualified_signature(node: ExprNode, skeleton_kind: str) -> str:
+    """`skeleton|signature`, the reference cache key (`codegen.py:268-270`)."""
+    return f"{skeleton_kind}|{signature_of(node)}"
+
+
+@dataclass
+class ReduceOutput:
+    kind: ReduceKind
+    out_id: int
+    etype: ElemType
+
+
+@dataclass
+class FusedKernelStep:
+    """One fused launch over a MatMul-free subtree."""
+
+    expr: ExprNode
+    skeleton: str
+    out_id: int
+    out_shape: MatShape
+    out_etype: ElemType
+    domain_shape: MatShape
+    signature: str
+    inputs: list[InputSpec]
+    scalars: list[ScalarSlot]
+    dim: int = 0
+    reductions: list[ReduceOutput] = field(default_factory=list)
+    finalize: int = FINAL_NONE
+
+    @classmethod
+    def create(cls, expr: ExprNode, skeleton: str, out_id: int,
+               finalize: int = FINAL_NONE) -> "FusedKernelStep":
+        inputs, scalars = collect_inputs(expr)
+        if skeleton == REDUCE_ACCU:
+            out_shape, out_etype = MatShape(1, 1), accumulator_type(expr.etype)
+        else:
+            out_shape, out_etype = expr.shape, expr.etype
+        sig = qualified_signature(expr, skeleton)
+        if finalize != FINAL_NONE:
+            sig += f"|final{finalize}"
+        return cls(expr, skeleton, out_id, out_shape, out_etype, expr.shape, sig,
+                   inputs, scalars, finalize=finalize)
+
+    @classmethod
+    def create_reduce(cls, child: ExprNode, dim: int,
+                      outputs: list[ReduceOutput]) -> "FusedKernelStep":
+        inputs, scalars = collect_inputs(child)
+        shape = MatShape(1, child.shape.n_cols) if dim == 0 else MatShape(child.shape.n_rows, 1)
+        kinds = ",".join(o.kind.value for o in outputs)
+        sig = f"{REDUCE_DIM}{{{dim}:{kinds}}}|{signature_of(child)}"
+        first = outputs[0]
+        return cls(child, REDUCE_DIM, first.out_id, shape, first.etype, child.shape, sig,
+                   inputs, scalars, dim=dim, reductions=list(outputs))
+
+
+@dataclass
+class GemmStep:
+    """out = alpha * op(A) @ op(B); op = transpose when the flag is set.
+    `a_shape`/`b_shape` are the STORED shapes of the dense operand buffers."""
+
+    a_id: int
+    b_id: int
+    out_id: int
+    a_shape: MatShape
+    b_shape: MatShape
+    trans_a: bool
+    trans_b: bool
+    alpha: float
+    in_etype: ElemType
+    out_etype: ElemType
+    out_shape: MatShape
+
+    @property
+    def m(self) -> int:
+        return self.out_shape.n_rows
+
+    @property
+    def n(self) -> int:
+        return self.out_shape.n_cols
+
+    @property
+    def k(self) -> int:
+        return self.a_shape.n_rows if self.trans_a else self.a_shape.n_cols
+
+    @property
+    def left_id(self) -> int:          # reference MatMulStep field names
+        return self.a_id
+
+    @property
+    def right_id(self) -> int:
+        return self.b_id
+
+
+# The reference's plain product step is a GemmStep with no folding.
+MatMulStep = GemmStep
+
+
+@dataclass
+class TempSpec:
+    temp_id: int
+    shape: MatShape
+    etype: ElemType
+
+
+@dataclass
+class ExecutionPlan:
+    steps: list
+    temps: list[TempSpec]
+    out_id: int
+    out_shape: MatShape
+    out_etype: ElemType
+    out_is_temp: bool = False
+
+    @property
+    def fused_steps(self) -> list[FusedKernelStep]:
+        return [s for s in self.steps if isinstance(s, FusedKernelStep)]
+
+    @property
+    def gemm_steps(self) -> list[GemmStep]:
+        return [s for s in self.steps if isinstance(s, GemmStep)]
+
+    matmul_steps = gemm_steps
+
+    def n_launches(self) -> int:
+        return len(self.steps)
+
+
+class _Planner:
+    def __init__(self) -> None:
+        self.steps: list = []
+        self.temps: list[TempSpec] = []
+        self._next = -1
+
+    def temp(self, shape: MatShape, etype: ElemType) -> TempSpec:
+        t = TempSpec(self._next, shape, etype)
+        self._next -= 1
+        self.temps.append(t)
+        return t
+
+    def materialize(self, node: ExprNode) -> Leaf:
+        node = self.split(node)
+        if isinstance(node, Leaf):
+            return node
+        t = self.temp(node.shape, node.etype)
+        self.steps.append(FusedKernelStep.create(node, COPY, t.temp_id))
+        return Leaf(t.temp_id, node.etype, node.shape)
+
+    def gemm_operand(self, node: ExprNode) -> tuple[Leaf, bool, float]:
+        """Peel scalar pre-multiplies and transposes off a product operand;
+        what remains is a dense leaf (used in place) or gets materialised."""
+        alpha, trans = 1.0, False
+        while True:
+            if isinstance(node, UnaryElem) and node.kind is UnaryKind.scalar_pre_mul:
+                alpha *= float(node.scalar)
+                node = node.child
+            elif isinstance(node, Transpose):
+                trans = not trans
+                node = node.child
+            else:
+                break
+        return self.materialize(node), trans, alpha
+
+    def gemm(self, node: MatMul, out_id: int | None = None) -> GemmStep:
+        a, ta, sa = self.gemm_operand(node.left)
+        b, tb, sb = self.gemm_operand(node.right)
+        if out_id is None:
+            out_id = self.temp(node.shape, node.etype).temp_id
+        step = GemmStep(a.mat_id, b.mat_id, out_id, a.shape, b.shape, ta, tb, sa * sb,
+                        a.etype, node.etype, node.shape)
+        self.steps.append(step)
+        return step
+
+    def split(self, node: ExprNode) -> ExprNode:
+        """Replace every MatMul / Reduce subtree with a dense temp leaf."""
+        if isinstance(node, MatMul):
+            step = self.gemm(node)
+            return Leaf(step.out_id, node.etype, node.shape)
+        if isinstance(node, Reduce):
+            child = self.split(node.child)
+            t = self.temp(node.shape, node.etype)
+            self.steps.append(FusedKernelStep.create_reduce(
+                child, node.dim, [ReduceOutput(node.kind, t.temp_id, node.etype)]))
+            return Leaf(t.temp_id, node.etype, node.shape)
+        if isinstance(node, (Leaf, Subview, Diag)):
+            return node
+        if isinstance(node, UnaryElem):
+            c = self.split(node.child)
+            if c is node.child:
+                return node
+            return UnaryElem(node.kind, c, scalar=node.scalar, exponent=node.exponent,
+                             target=node.target)
+        if isinstance(node, BinaryElem):
+            a, b = self.split(node.left), self.split(node.right)
+            if a is node.left and b is node.right:
+                return node
+            return BinaryElem(node.kind, a, b)
+        if isinstance(node, Transpose):
+            c = self.split(node.child)
+            return node if c is node.child else Transpose(c)
+        raise PlanError(f"cannot plan node {type(node).__name__}")
+
+
+def plan(out_mat_id: int, node: ExprNode) -> ExecutionPlan:
+    """Plan `out = node` (`plan.py:171-205` semantics plus folding)."""
+    p = _Planner()
+    unsafe = aliases(out_mat_id, node) is AliasKind.UNSAFE
+
+    if isinstance(node, MatMul):
+        target = p.temp(node.shape, node.etype).temp_id if unsafe else out_mat_id
+        p.gemm(node, target)
+        return ExecutionPlan(p.steps, p.temps, target, node.shape, node.etype,
+                             out_is_temp=unsafe)
+
+    if isinstance(node, Reduce):
+        child = p.split(node.child)
+        target = p.temp(node.shape, node.etype).temp_id if unsafe else out_mat_id
+        p.steps.append(FusedKernelStep.create_reduce(
+            child, node.dim, [ReduceOutput(node.kind, target, node.etype)]))
+        return ExecutionPlan(p.steps, p.temps, target, node.shape, node.etype,
+                             out_is_temp=unsafe)
+
+    root = p.split(node)
+    if unsafe:
+        t = p.temp(root.shape, root.etype)
+        p.steps.append(FusedKernelStep.create(root, COPY, t.temp_id))
+        return ExecutionPlan(p.steps, p.temps, t.temp_id, root.shape, root.etype,
+                             out_is_temp=True)
+    p.steps.append(FusedKernelStep.create(root, COPY, out_mat_id))
+    return ExecutionPlan(p.steps, p.temps, out_mat_id, root.shape, root.etype)
+
+
+def reduce_plan(node: ExprNode, finalize: int = FINAL_NONE) -> ExecutionPlan:
+    """Full reduction into a 1x1 accumulator temp (`plan.py:208-215`)."""
+    p = _Planner()
+    root = p.split(node)
+    acc = p.temp(MatShape(1, 1), accumulator_type(root.etype))
+    p.steps.append(FusedKernelStep.create(root, REDUCE_ACCU, acc.temp_id, finalize))
+    return ExecutionPlan(p.steps, p.temps, acc.temp_id, acc.shape, acc.etype,
+                         out_is_temp=True)
+
+
+def _binding_key(node: ExprNode):
+    """Structure plus concrete bindings: two reductions can share a launch iff
+    they read the same matrices through the same maps with the same scalars."""
+    inputs, scalars = collect_inputs(node)
+    return (signature_of(node),
+            tuple((s.mat_id, tuple((v.kind, v.row_off, v.col_off) for v in s.views))
+                  for s in inputs),
+            tuple(s.value for s in scalars))
+
+
+def plan_many(assignments: list[tuple[int, ExprNode]]) -> ExecutionPlan:
+    """Plan several assignments together.  Reduce roots along the same dim of
+    the same bound subexpression fuse into one multi-output launch (C4's
+    sum/mean/max/index_max read X, Y, Z once); everything else plans as
+    `plan` would, in order.  Outputs must not alias any input."""
+    p = _Planner()
+    groups: dict = {}
+    order: list = []
+    for out_id, node in assignments:
+        if aliases(out_id, node) is not AliasKind.NONE:
+            raise PlanError("plan_many outputs may not alias their inputs")
+        if isinstance(node, Reduce):
+            key = (node.dim, _binding_key(node.child))
+            if key not in groups:
+                groups[key] = (node, [])
+                order.append(key)
+            groups[key][1].append(ReduceOutput(node.kind, out_id, node.etype))
+        else:
+            order.append((out_id, node))
+    for item in order:
+        if item in groups:
+            node, outs = groups[item]
+            child = p.split(node.child)
+            p.steps.append(FusedKernelStep.create_reduce(child, node.dim, outs))
+        else:
+            out_id, node = item
+            if isinstance(node, MatMul):
+                p.gemm(node, out_id)
+            else:
+                root = p.split(node)
+                p.steps.append(FusedKernelStep.create(root, COPY, out_id))
+    last = assignments[-1]
+    return ExecutionPlan(p.steps, p.temps, last[0], last[1].shape, last[1].etype)

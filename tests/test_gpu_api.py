@@ -1,0 +1,325 @@
+"""User API semantics on the GPU, mirroring the reference's test_matrix.py /
+test_backend.py known answers (/root/reference/pkg/tests)."""
+
+import numpy as np
+import pytest
+
+import paper_2604_22242_b200 as fm
+from oracle import fm_oracle as orc
+from paper_2604_22242_b200.errors import BackendError, FusematError, OutOfBoundsError, ShapeError
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def ctx(gpu_ctx):
+    return fm.Context(gpu_ctx.backend)
+
+
+# --- constructors (test_matrix.py:20-62) ------------------------------------------
+def test_zeros_ones_fill(ctx):
+    assert fm.zeros(2, 2, ctx=ctx).to_numpy().tolist() == [[0, 0], [0, 0]]
+    assert fm.fill(1, 3, 7, ctx=ctx).to_numpy().tolist() == [[7, 7, 7]]
+    assert fm.ones(2, 3, ctx=ctx).to_numpy().sum() == 6
+    assert fm.fill(2, 2, -3, "i32", ctx=ctx).to_numpy().tolist() == [[-3, -3], [-3, -3]]
+    assert fm.fill(1, 2, 2.5, "f64", ctx=ctx).to_numpy().tolist() == [[2.5, 2.5]]
+
+
+@pytest.mark.parametrize("etype", ["f32", "f64", "bf16"])
+def test_device_randu_bit_exact_with_reference_stream(ctx, etype):
+    for seed in (42, 43, 2**63 + 5):
+        m = fm.randu(37, 29, seed, etype, ctx=ctx)
+        assert np.array_equal(m.to_numpy(), orc.randu(37, 29, seed, etype))
+
+
+def test_device_randi(ctx):
+    y = fm.randi(64, 64, 10, seed=1, ctx=ctx)
+    want = orc.uniform_int_fill(1, 64 * 64, "u32", 10).reshape(64, 64, order="F")
+    assert np.array_equal(y.to_numpy(), want)
+
+
+def test_from_array_roundtrip(ctx):
+    for dt in (np.float32, np.float64, np.int32, np.uint32):
+        a = (np.arange(12).reshape(3, 4) * 3 - 5).astype(dt)
+        assert np.array_equal(fm.from_array(a, ctx=ctx).to_numpy(), a)
+
+
+# --- assignment and caching (test_matrix.py:75-130) ---------------------------------
+def test_assign_then_read(ctx):
+    x = fm.from_array(np.array([[1, 2], [3, 4]], np.float32), ctx=ctx)
+    y = fm.from_array(np.array([[5, 6], [7, 8]], np.float32), ctx=ctx)
+    z = fm.zeros(2, 2, ctx=ctx)
+    z.assign(x + y)
+    assert z[0, 0] == 6
+    assert z.to_numpy().tolist() == [[6, 8], [10, 12]]
+
+
+def test_scalar_variants_share_kernel(ctx):
+    x = fm.randu(4, 4, seed=1, ctx=ctx)
+    z = fm.zeros(4, 4, ctx=ctx)
+    ctx.reset_counters()
+    z.assign(x + 3.0)
+    z.assign(x + 5.0)
+    assert ctx.compile_count == 1 and ctx.launches == 2
+    assert np.array_equal(z.to_numpy(), x.to_numpy() + np.float32(5))
+
+
+def test_fifty_trials_after_two_warmups(ctx):
+    x = fm.randu(8, 8, seed=1, ctx=ctx)
+    y = fm.randu(8, 8, seed=2, ctx=ctx)
+    z = fm.zeros(8, 8, ctx=ctx)
+    e = x + y
+    ctx.reset_counters()
+    for _ in range(52):
+        z.assign(e)
+    assert ctx.compile_count == 1 and ctx.launches == 52
+
+
+def test_add4_single_launch(ctx):
+    mats = [fm.randu(8, 8, seed=i, ctx=ctx) for i in range(4)]
+    z = fm.zeros(8, 8, ctx=ctx)
+    ctx.reset_counters()
+    z.assign(mats[0] + mats[1] + mats[2] + mats[3])
+    assert ctx.launches == 1
+    a = [m.to_numpy() for m in mats]
+    assert np.array_equal(z.to_numpy(), ((a[0] + a[1]) + a[2]) + a[3])
+
+
+def test_long_chain_addn_single_launch(ctx):
+    mats = [fm.randu(33, 17, seed=i, ctx=ctx) for i in range(32)]
+    e = mats[0] + mats[1]
+    for m in mats[2:]:
+        e = e + m
+    z = fm.zeros(33, 17, ctx=ctx)
+    ctx.reset_counters()
+    z.assign(e)
+    assert ctx.launches == 1
+    want = mats[0].to_numpy() + mats[1].to_numpy()
+    for m in mats[2:]:
+        want = want + m.to_numpy()
+    assert np.array_equal(z.to_numpy(), want)
+
+
+# --- element access ------------------------------------------------------------------
+def test_elem_get_set_bounds(ctx):
+    m = fm.zeros(3, 3, ctx=ctx)
+    m[1, 2] = 42.0
+    assert m[1, 2] == 42.0
+    with pytest.raises(OutOfBoundsError):
+        m.elem_get(3, 0)
+
+
+# --- reductions (test_matrix.py:139-185) ------------------------------------------------
+def test_accu_known_answers(ctx):
+    assert fm.accu(fm.ones(3, 3, ctx=ctx)) == 9.0
+    x = fm.from_array(np.array([[1, 2], [3, 4]], np.float32), ctx=ctx)
+    assert fm.accu(x) == 10.0
+    r = fm.randu(5, 5, seed=9, ctx=ctx)
+    assert fm.accu(r - r) == 0.0
+    y = fm.from_array(np.array([[-3, 1], [2, -5]], np.float32), ctx=ctx)
+    assert fm.accu(y * (y > 0)) == 3.0
+    assert fm.accu(fm.zeros(7, 3, ctx=ctx)) == 0.0
+    big = fm.fill(2, 1, 2**31, "u32", ctx=ctx)
+    assert fm.accu(big) == 0
+
+
+def test_accu_fuses_and_accumulates_in_f64(ctx):
+    x = fm.randu(4, 4, seed=1, ctx=ctx)
+    y = fm.randu(4, 4, seed=2, ctx=ctx)
+    ctx.reset_counters()
+    total = fm.accu(x + y)
+    assert ctx.launches == 1
+    assert total == pytest.approx(float((x.to_numpy() + y.to_numpy()).astype(np.float64).sum()), rel=1e-12)
+
+
+def test_accu_of_matmul_splits(ctx):
+    a = fm.randu(3, 4, seed=1, ctx=ctx)
+    b = fm.randu(4, 2, seed=2, ctx=ctx)
+    total = fm.accu(a @ b)
+    assert total == pytest.approx(float((a.to_numpy().astype(np.float64) @ b.to_numpy()).sum()), rel=1e-5)
+
+
+def test_dot_and_norm(ctx):
+    x = fm.Col(1000, ctx=ctx)
+    x.assign(fm.randu(1000, 1, 3, ctx=ctx))
+    y = fm.randu(1000, 1, 4, ctx=ctx)
+    xn, yn = x.to_numpy(), y.to_numpy()
+    assert fm.dot(x, y) == pytest.approx(orc.accu(xn * yn, fm.ElemType.f32), rel=1e-12)
+    d = xn - yn
+    assert fm.norm(x - y) == pytest.approx(np.sqrt(orc.accu(d * d, fm.ElemType.f32)), rel=1e-12)
+
+
+@pytest.mark.parametrize("etype", ["f32", "f64", "i32", "u32"])
+@pytest.mark.parametrize("dim", [0, 1])
+@pytest.mark.parametrize("shape", [(1, 1), (5, 3), (37, 129), (1000, 7), (4, 1500)])
+def test_dim_reductions(ctx, etype, dim, shape):
+    n_rows, n_cols = shape
+    rng = np.random.default_rng(n_rows * 31 + n_cols)
+    if etype in ("f32", "f64"):
+        a = rng.integers(-4, 5, size=shape).astype(etype.replace("f", "float"))  # ties on purpose
+    else:
+        a = rng.integers(-4 if etype == "i32" else 0, 9, size=shape).astype("int32" if etype == "i32" else "uint32")
+    X = fm.from_array(a, ctx=ctx)
+    ety = fm.ElemType.of(etype)
+    kinds = [(fm.sum, orc.ReduceKind.sum), (fm.max, orc.ReduceKind.max), (fm.min, orc.ReduceKind.min),
+             (fm.index_max, orc.ReduceKind.index_max), (fm.index_min, orc.ReduceKind.index_min)]
+    if ety.is_float:
+        kinds.append((fm.mean, orc.ReduceKind.mean))
+    for fn, kind in kinds:
+        got = fn(X, dim).eval().to_numpy()
+        want = orc.reduce_dim(kind, dim, a, ety)
+        assert np.array_equal(got, want), (fn.__name__, etype, dim, shape)
+
+
+def test_dim_reductions_nan_first_index(ctx):
+    a = np.array([[1.0, 2.0], [np.nan, 5.0], [np.nan, 5.0]], np.float64)
+    X = fm.from_array(a, ctx=ctx)
+    assert fm.index_max(X, 0).eval().to_numpy().tolist() == [[1, 1]]
+    assert np.isnan(fm.max(X, 0).eval().to_numpy()[0, 0])
+
+
+def test_assign_all_fuses_reductions_into_one_launch(ctx):
+    X = fm.randu(300, 40, 42, "f64", ctx=ctx)
+    Y = fm.randu(300, 40, 43, "f64", ctx=ctx)
+    Z = fm.randu(300, 40, 44, "f64", ctx=ctx)
+    e = (X - Y) % Z
+    s, m, mx, im = (fm.Mat(1, 40, "f64", ctx), fm.Mat(1, 40, "f64", ctx),
+                    fm.Mat(1, 40, "f64", ctx), fm.Mat(1, 40, "u32", ctx))
+    ctx.reset_counters()
+    fm.assign_all([(s, fm.sum(e, 0)), (m, fm.mean(e, 0)), (mx, fm.max(e, 0)), (im, fm.index_max(e, 0))])
+    assert ctx.launches == 1
+    v = (X.to_numpy() - Y.to_numpy()) * Z.to_numpy()
+    k = orc.ReduceKind
+    assert np.allclose(s.to_numpy(), orc.reduce_dim(k.sum, 0, v, fm.ElemType.f64), rtol=1e-13, atol=0)
+    assert np.allclose(m.to_numpy(), orc.reduce_dim(k.mean, 0, v, fm.ElemType.f64), rtol=1e-13, atol=0)
+    assert np.array_equal(mx.to_numpy(), orc.reduce_dim(k.max, 0, v, fm.ElemType.f64))
+    assert np.array_equal(im.to_numpy(), orc.reduce_dim(k.index_max, 0, v, fm.ElemType.f64))
+
+
+# --- conversions (test_matrix.py:189-214) ------------------------------------------------
+def test_conversions(ctx):
+    y = fm.from_array(np.array([[1, 2, 3]], np.uint32), ctx=ctx)
+    z = fm.zeros(1, 3, ctx=ctx)
+    z.assign(fm.conv_to(y, "f32"))
+    assert z.to_numpy().tolist() == [[1.0, 2.0, 3.0]]
+    x = fm.from_array(np.array([[2.9, -2.9, np.nan, 3e10]], np.float32), ctx=ctx)
+    zi = fm.zeros(1, 4, "i32", ctx=ctx)
+    zi.assign(fm.conv_to(x, "i32"))
+    assert zi.to_numpy().tolist() == orc.materialize(fm.conv_to(x, "i32").node, {x.mat_id: x.to_numpy()}).tolist()
+    zu = fm.zeros(1, 4, "u32", ctx=ctx)
+    zu.assign(fm.conv_to(x, "u32"))
+    assert zu.to_numpy()[0, 1] == 2**32 - 2
+
+
+def test_bf16_roundtrip_and_ops(ctx):
+    a = np.linspace(-3, 3, 64, dtype=np.float32).reshape(8, 8)
+    X = fm.from_array(a, etype="bf16", ctx=ctx)
+    assert np.array_equal(X.to_numpy(), orc.bf16_round(a))
+    e = 2.5 * X + X
+    got = e.eval().to_numpy()
+    want = orc.materialize(e.node, {X.mat_id: orc.bf16_round(a)})
+    assert np.array_equal(got, want)
+    f = fm.conv_to(X, "f32")
+    assert np.array_equal(f.eval().to_numpy(), orc.bf16_round(a))
+
+
+def test_mixed_types_without_conv_rejected(ctx):
+    x = fm.randu(2, 2, seed=1, ctx=ctx)
+    y = fm.randi(2, 2, 10, seed=2, ctx=ctx)
+    with pytest.raises(ShapeError):
+        x + y
+
+
+# --- aliasing, resizing, async ---------------------------------------------------------------
+def test_safe_alias_in_place(ctx):
+    z = fm.randu(64, 64, seed=5, ctx=ctx)
+    y = fm.randu(64, 64, seed=6, ctx=ctx)
+    before = z.to_numpy()
+    z.assign(z + y)
+    assert np.array_equal(z.to_numpy(), before + y.to_numpy())
+
+
+def test_unsafe_alias_transposed_self(ctx):
+    z = fm.randu(40, 40, seed=7, ctx=ctx)
+    y = fm.randu(40, 40, seed=8, ctx=ctx)
+    snap = z.to_numpy()
+    z.assign(z.t() + y)
+    assert np.array_equal(z.to_numpy(), snap.T + y.to_numpy())
+
+
+def test_unsafe_alias_matmul_self(ctx):
+    z = fm.randu(3, 3, seed=9, ctx=ctx)
+    snap = z.to_numpy().astype(np.float64)
+    z.assign(z @ z)
+    assert np.allclose(z.to_numpy(), (snap @ snap).astype(np.float32), atol=1e-6)
+
+
+def test_assign_resizes_output(ctx):
+    x = fm.randu(5, 3, seed=1, ctx=ctx)
+    z = fm.zeros(2, 2, ctx=ctx)
+    z.assign(x + 0.5)
+    assert z.shape == fm.MatShape(5, 3)
+
+
+def test_async_unobservable(ctx):
+    x = fm.randu(600, 600, seed=3, ctx=ctx)
+    z = fm.zeros(600, 600, ctx=ctx)
+    z.assign(x + 1.0)
+    z.assign(z * 2.0)
+    assert np.array_equal(z.to_numpy(), (x.to_numpy() + np.float32(1)) * np.float32(2))
+
+
+def test_views_subview_diag(ctx):
+    a = orc.randu(20, 20, 11)
+    b = orc.randu(20, 20, 12)
+    A, B = fm.from_array(a, ctx=ctx), fm.from_array(b, ctx=ctx)
+    e = A.center_half() + B.center_half()
+    assert np.array_equal(e.eval().to_numpy(), a[5:15, 5:15] + b[5:15, 5:15])
+    d = (A.diag(-1) + A.diag(1)) % (B.diag(-1) + B.diag(1))
+    want = (np.diagonal(a, -1) + np.diagonal(a, 1)) * (np.diagonal(b, -1) + np.diagonal(b, 1))
+    assert np.array_equal(d.eval().to_numpy().ravel(), want)
+
+
+# --- backend contract errors (test_backend.py:24-57, test_cjit.py:41-60) --------------------------
+def test_buffer_contract(gpu_ctx):
+    be = gpu_ctx.backend
+    h = be.alloc(fm.ElemType.i32, 8)
+    assert be.download(h).tolist() == [0] * 8           # zero-initialised
+    be.upload(np.arange(8, dtype=np.int32), h)
+    assert be.download(h).tolist() == list(range(8))
+    with pytest.raises(BackendError):
+        be.upload(np.zeros(5, np.int32), h)
+    be.free(h)
+    with pytest.raises(BackendError):
+        be.free(h)
+    with pytest.raises(BackendError):
+        be.download(h)
+    e = be.alloc(fm.ElemType.f32, 0)
+    assert be.download(e).size == 0
+
+
+def test_launch_schema_errors(gpu_ctx):
+    from paper_2604_22242_b200 import exprtree as ast
+    from paper_2604_22242_b200.backend import make_kernel_source
+    be = gpu_ctx.backend
+    node = ast.plus(ast.leaf(0, "f32", fm.MatShape(2, 2)), ast.leaf(1, "f32", fm.MatShape(2, 2)))
+    k = be.compile(make_kernel_source(node, "copy", "copy|" + ast.signature_of(node)))
+    with pytest.raises(fm.SchemaError):
+        be.launch(k, [be.alloc(fm.ElemType.f32, 4), 2, 2], (2, 2))
+    a, b = be.alloc(fm.ElemType.f32, 4), be.alloc(fm.ElemType.f64, 4)
+    with pytest.raises(fm.SchemaError):
+        be.launch(k, [be.alloc(fm.ElemType.f32, 4), 2, 2, a, 2, 2, b, 2, 2], (2, 2))
+
+
+def test_context_mixing_rejected(gpu_ctx):
+    other = fm.Context(gpu_ctx.backend)
+    x = fm.randu(2, 2, seed=1, ctx=gpu_ctx)
+    y = fm.randu(2, 2, seed=1, ctx=other)
+    with pytest.raises(FusematError):
+        x + y
+
+
+def test_save_load_roundtrip(ctx, tmp_path):
+    m = fm.randu(5, 4, seed=11, ctx=ctx)
+    fm.save_matrix(m, tmp_path / "m.txt")
+    assert np.array_equal(fm.load_matrix(tmp_path / "m.txt", ctx=ctx).to_numpy(), m.to_numpy())

@@ -1,0 +1,179 @@
+"""Host-side logic on CPU: expression trees, signatures (byte-compatible with
+the reference), planning (fusion extent, GEMM folding, reductions, aliasing)
+and lowering to the fused program.  Mirrors the reference's test_expr.py /
+test_plan.py / test_codegen.py."""
+
+import pytest
+
+from paper_2604_22242_b200 import exprtree as ast
+from paper_2604_22242_b200 import lower, plan as P
+from paper_2604_22242_b200.aot_registry import hot_expressions, registered_signatures
+from paper_2604_22242_b200.backend import arg_schema
+from paper_2604_22242_b200.errors import GenerationError, OutOfBoundsError, ShapeError
+from paper_2604_22242_b200.exprtree import ElemType, MatShape
+from treeio import from_json
+
+F32, F64 = ElemType.f32, ElemType.f64
+OUT = 999
+
+
+def L(i, r=8, c=8, t=F32):
+    return ast.leaf(i, t, MatShape(r, c))
+
+
+# --- signatures & schemas match the reference byte for byte ------------------------------
+def test_signatures_match_reference(golden_signatures):
+    for row in golden_signatures:
+        node = from_json(row["tree"])
+        assert ast.signature_of(node) == row["signature"], row["name"]
+        if "qualified_copy" in row:
+            assert P.qualified_signature(node, P.COPY) == row["qualified_copy"]
+            assert P.qualified_signature(node, P.REDUCE_ACCU) == row["qualified_accu"]
+            assert [str(a) for a in arg_schema(node, P.COPY)] == row["schema_copy"]
+            assert [str(a) for a in arg_schema(node, P.REDUCE_ACCU)] == row["schema_accu"]
+        inputs, slots = ast.collect_inputs(node)
+        assert [s.mat_id for s in inputs] == row["inputs"]
+        assert [s.value for s in slots] == row["slots"]
+
+
+def test_signature_ignores_scalars_and_ids():
+    a = ast.scalar_add(L(0), 3.0)
+    b = ast.scalar_add(L(7), 5.0)
+    assert ast.signature_of(a) == ast.signature_of(b)
+    assert ast.signature_of(ast.plus(L(0), L(0))) != ast.signature_of(ast.plus(L(0), L(1)))
+
+
+def test_conformability_and_types():
+    with pytest.raises(ShapeError):
+        ast.plus(L(0, 2, 2), L(1, 2, 3))
+    with pytest.raises(ShapeError):
+        ast.plus(L(0), L(1, t=F64))
+    with pytest.raises(ShapeError):
+        ast.exp(L(0, t=ElemType.i32))
+    with pytest.raises(ShapeError):
+        ast.pow_int(L(0), 17)
+    with pytest.raises(OutOfBoundsError):
+        ast.subview(0, F32, 3, 0, MatShape(2, 2), MatShape(4, 4))
+    with pytest.raises(ShapeError):
+        ast.scalar_add(L(0, t=ElemType.i32), 1.5)
+    assert ast.matmul(L(0, 4, 3, ElemType.bf16), L(1, 3, 5, ElemType.bf16)).etype is F32
+    assert ast.reduce(ast.ReduceKind.index_max, 0, L(0, 5, 7)).shape == MatShape(1, 7)
+    assert ast.reduce(ast.ReduceKind.sum, 1, L(0, 5, 7)).shape == MatShape(5, 1)
+    with pytest.raises(ShapeError):
+        ast.reduce(ast.ReduceKind.mean, 0, L(0, t=ElemType.u32))
+
+
+# --- planning ----------------------------------------------------------------------------------
+def test_elementwise_is_one_step():
+    pl = P.plan(OUT, ast.plus(L(0), L(1)))
+    assert len(pl.steps) == 1 and pl.steps[0].out_id == OUT and not pl.temps
+
+
+def test_c5_gemm_folds_scalar_and_transpose_into_one_launch():
+    X, Y = L(0, 64, 32), L(1, 48, 32)
+    node = ast.matmul(ast.scalar_pre_mul(2, X), ast.transpose(Y))   # 2 * X @ Y.t()
+    pl = P.plan(OUT, node)
+    assert len(pl.steps) == 1 and not pl.temps
+    g = pl.steps[0]
+    assert isinstance(g, P.GemmStep)
+    assert (g.a_id, g.b_id, g.trans_a, g.trans_b, g.alpha) == (0, 1, False, True, 2.0)
+    assert (g.m, g.n, g.k) == (64, 48, 32) and g.out_id == OUT
+
+
+def test_gemm_operand_expression_materialised_once():
+    node = ast.matmul(ast.transpose(ast.plus(L(0, 4, 8), L(1, 4, 8))), L(2, 4, 2))
+    pl = P.plan(OUT, node)
+    assert len(pl.fused_steps) == 1 and len(pl.gemm_steps) == 1
+    assert pl.fused_steps[0].out_shape == MatShape(4, 8)      # no transpose copy
+    assert pl.gemm_steps[0].trans_a
+
+
+def test_chain_three_gemms_left_to_right():
+    a, b, c, d = L(0, 16, 8), L(1, 8, 4), L(2, 4, 2), L(3, 2, 1)
+    pl = P.plan(OUT, ast.matmul(ast.matmul(ast.matmul(a, b), c), d))
+    assert len(pl.gemm_steps) == 3 and pl.gemm_steps[-1].out_id == OUT and len(pl.temps) == 2
+
+
+def test_alias_handling():
+    assert not P.plan(OUT, ast.plus(L(OUT), L(1))).out_is_temp
+    pl = P.plan(OUT, ast.plus(ast.transpose(L(OUT)), L(1)))
+    assert pl.out_is_temp and len(pl.fused_steps) == 1
+    assert P.plan(OUT, ast.matmul(L(OUT), L(1))).out_is_temp
+
+
+def test_reduce_root_single_step_and_multi_output_fusion():
+    e = ast.schur(ast.minus(L(0, t=F64), L(1, t=F64)), L(2, t=F64))
+    outs = [(10, ast.reduce(ast.ReduceKind.sum, 0, e)), (11, ast.reduce(ast.ReduceKind.mean, 0, e)),
+            (12, ast.reduce(ast.ReduceKind.max, 0, e)), (13, ast.reduce(ast.ReduceKind.index_max, 0, e))]
+    pl = P.plan_many(outs)
+    assert len(pl.steps) == 1
+    assert [o.out_id for o in pl.steps[0].reductions] == [10, 11, 12, 13]
+    # different dims do not fuse
+    pl2 = P.plan_many(outs[:1] + [(14, ast.reduce(ast.ReduceKind.sum, 1, e))])
+    assert len(pl2.steps) == 2
+
+
+def test_reduce_inside_expression_is_a_barrier():
+    r = ast.reduce(ast.ReduceKind.sum, 0, L(0, 4, 6))
+    pl = P.plan(OUT, ast.scalar_add(r, 1.0))
+    assert len(pl.steps) == 2 and pl.steps[0].skeleton == P.REDUCE_DIM
+
+
+# --- lowering ----------------------------------------------------------------------------------
+def test_c1_program():
+    node = ast.plus(ast.scalar_pre_mul(2, ast.schur(L(0), L(1))), L(0))
+    p = lower.lower(node)
+    assert p.flat and p.depth == 2 and len(p.slots) == 2
+    assert p.disassemble() == ["PUSH32@0 0", "PUSH32@1 1", "MUL_F@0 0", "SMUL_F@0 0",
+                               "PUSH32@1 0", "ADD_F@0 0"]
+
+
+def test_sethi_ullman_keeps_deep_trees_shallow():
+    leaves = [L(i % 8) for i in range(64)]
+    while len(leaves) > 1:                       # balanced 64-leaf tree needs 7 registers
+        leaves = [ast.minus(leaves[i], leaves[i + 1]) for i in range(0, len(leaves), 2)]
+    p = lower.lower(leaves[0])
+    assert p.depth == 7
+    chain = L(0)
+    for i in range(1, 40):                       # left-deep addN needs 2
+        chain = ast.plus(chain, L(i))
+    assert lower.lower(chain).depth == 2
+
+
+def test_right_heavy_subtraction_uses_reversed_opcode():
+    node = ast.minus(L(0), ast.plus(L(1), L(2)))
+    p = lower.lower(node)
+    assert p.disassemble()[-1] == "RSUB_F@0 0"
+
+
+def test_views_and_transposes_are_not_flat():
+    sv = ast.subview(0, F32, 1, 1, MatShape(4, 4), MatShape(8, 8))
+    assert not lower.lower(ast.plus(sv, L(1, 4, 4))).flat
+    assert not lower.lower(ast.plus(ast.transpose(L(0)), L(1))).flat
+
+
+def test_lowering_limits():
+    big = L(0)
+    for i in range(1, 45):
+        big = ast.plus(big, L(i))
+    with pytest.raises(GenerationError):
+        lower.lower(big)
+
+
+def test_bf16_nodes_round_after_every_op():
+    x = L(0, t=ElemType.bf16)
+    p = lower.lower(ast.plus(ast.scalar_pre_mul(2.5, x), x))
+    assert [s.split("@")[0] for s in p.disassemble()].count("RND_BF_F") == 2
+
+
+def test_aot_registry_covers_the_configs():
+    sigs = set(registered_signatures())
+    X, Y, Z = L(0), L(1), L(2)
+    c1 = ast.plus(ast.scalar_pre_mul(2, ast.schur(X, Y)), X)
+    c3 = ast.plus(ast.exp(ast.scalar_pre_mul(0.5, ast.neg(ast.square(ast.minus(X, Y))))),
+                  ast.scalar_pre_mul(0.5, ast.abs_(X)))
+    X64, Y64, Z64 = L(0, t=F64), L(1, t=F64), L(2, t=F64)
+    for n in (c1, c3, ast.schur(X, Y), ast.square(ast.minus(X, Y)),
+              ast.schur(ast.minus(X64, Y64), Z64), ast.schur(X64, Y64)):
+        assert ast.signature_of(n) in sigs
+    assert len(hot_expressions()) == len(sigs)
