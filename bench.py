@@ -648,7 +648,7 @@ def ours(args, d: Dist):
             "config": {"workload": cfg.workload,
                        "elements_per_gpu_per_step": cfg.elements_per_step(),
                        "algorithmic_bytes_per_gpu_per_step": cfg.bytes_per_step(),
-                       "l2": ("L2 flushed (512 MiB write) before every timed step" if flush_h is not None
+                       "l2": ("L2 flushed before every timed step: 512 MiB write then a read of the same buffer (inputs evicted, no dirty lines left to write back inside the timed kernel)" if flush_h is not None
                               else "inputs larger than the 126 MB L2; no flush"),
                        "parallelism": f"column/slice sharded x{d.world}, one process per GPU"
                                       + (", one NCCL all_reduce of partials per step" if cfg.name == "c2" and d.world > 1 else "")},

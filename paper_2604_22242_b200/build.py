@@ -26,7 +26,25 @@ LIB = PKG / "libfmb200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-v", "-I", str(INCLUDE), "-I", str(CSRC)]
-SOURCES = ["runtime.cu", "fused.cu", "gen_templates.cu", "rng.cu", "gemm_simt.cu", "gemm_tc.cu"]
+SOURCES = ["runtime.cu", "fused.cu", "rng.cu", "gemm_simt.cu", "gemm_tc.cu"]
+
+
+def units() -> list[tuple[str, str, list[str]]]:
+    """(object stem, source, extra defines) of every compilation unit.
+
+    The two heavy sources are compiled several times with different macros so
+    nvcc runs them in parallel: the register-VM kernels once per (variant,
+    skeleton) and the expression-template kernels once per shard.
+    """
+    from .aot_registry import TEMPLATE_SHARDS
+    out = [(Path(s).stem, s, []) for s in SOURCES]
+    for v in range(4):
+        for k in range(3):
+            out.append((f"vm_inst_{v}_{k}", "vm_inst.cu", [f"-DFM_VM_VARIANT={v}", f"-DFM_VM_SKELETON={k}"]))
+    for k in range(TEMPLATE_SHARDS):
+        out.append((f"gen_templates_{k}", "gen_templates.cu",
+                    [f"-DFM_TEMPLATE_SHARD={k}", f"-DFM_TEMPLATE_SHARDS={TEMPLATE_SHARDS}"]))
+    return out
 
 
 def nvcc() -> str:
@@ -41,13 +59,13 @@ def _deps_mtime() -> float:
     return max(f.stat().st_mtime for f in files)
 
 
-def _compile(src: Path, obj: Path, verbose: bool) -> str:
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+def _compile(src: Path, obj: Path, defines: list[str], verbose: bool) -> str:
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *defines, "-c", str(src), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr[-6000:]}")
     (obj.with_suffix(".ptxas.txt")).write_text(r.stderr)
-    return src.name
+    return obj.stem
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -57,18 +75,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     dep = _deps_mtime()
     jobs = []
     objs = []
-    for name in SOURCES:
+    for stem, name, defines in units():
         src = CSRC / name
-        obj = BUILD / (src.stem + ".o")
+        obj = BUILD / (stem + ".o")
         objs.append(obj)
         if force or not obj.exists() or obj.stat().st_mtime < max(src.stat().st_mtime, dep):
-            jobs.append((src, obj))
+            jobs.append((src, obj, defines))
     if jobs:
         workers = min(len(jobs), os.cpu_count() or 4)
         with ThreadPoolExecutor(max_workers=workers) as ex:
-            for name in ex.map(lambda j: _compile(j[0], j[1], verbose), jobs):
+            for name in ex.map(lambda j: _compile(j[0], j[1], j[2], verbose), jobs):
                 if verbose:
                     print(f"  compiled {name}", file=sys.stderr)
+    for stale in BUILD.glob("*.o"):
+        if stale not in objs:
+            stale.unlink()
     if force or jobs or not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
         tmp = LIB.with_suffix(".so.tmp")
         cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs),

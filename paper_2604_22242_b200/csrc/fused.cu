@@ -9,16 +9,9 @@
 #include <cstring>
 #include <string>
 
-#include "launch.cuh"
+#include "vm_variants.cuh"
 
 namespace fm {
-
-// VM variants: 64-bit registers only when the program touches f64; a
-// shallower stack when the program allows (fewer live registers).
-using Vm32s = Vm<false, 4, 8, 4>;
-using Vm32d = Vm<false, 8, 8, 4>;
-using Vm64s = Vm<true, 4, 4, 4>;
-using Vm64d = Vm<true, 8, 4, 4>;
 
 static int validate(const fm_program *P) {
   if (!P) return fail_msg("null program");

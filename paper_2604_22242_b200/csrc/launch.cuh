@@ -11,13 +11,35 @@ namespace fm {
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Resident blocks of `kernel` per SM at kThreads threads (queried once per
+// kernel).  Streaming kernels launch exactly one full wave -- SMs x resident
+// blocks -- and grid-stride: a fractional last wave would leave most SMs idle
+// while a few finish (ncu showed 1.33 and 5.33 waves before this).
+// `Tag` keys the cache: every k_copy<E> has the same function-pointer type.
+template <class Tag, class K>
+int resident_blocks(K kernel) {
+  static int cached = 0;
+  if (cached == 0) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kThreads, 0) != cudaSuccess || n < 1) n = 1;
+    cached = n;
+  }
+  return cached;
+}
+template <class Tag, class K>
+int64_t wave_grid(K kernel, int64_t work_blocks) {
+  const int64_t full = (int64_t)sm_count() * resident_blocks<Tag>(kernel);
+  return std::max<int64_t>(1, std::min<int64_t>(work_blocks, full));
+}
+template <class E, int Skel> struct GridTag {};
+
 template <class E>
 int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s) {
   constexpr int V = E::kV;
   if (n_rows == 0 || n_cols == 0) return 0;
   const int64_t nrb = cdiv(n_rows, V);
   const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;
-  const int64_t grid = std::min<int64_t>(cdiv(nch, kThreads), (int64_t)sm_count() * 32);
+  const int64_t grid = wave_grid<GridTag<E, 0>>(k_copy<E>, cdiv(nch, kThreads));
   k_copy<E><<<(unsigned)grid, kThreads, 0, s>>>(P, out, n_rows, n_cols);
   FM_CHECK_LAUNCH("fused copy kernel");
   return 0;
@@ -29,7 +51,7 @@ int run_accu(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, int
   constexpr int V = E::kV;
   const int64_t nrb = cdiv(n_rows, V);
   const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(cdiv(nch, kThreads), (int64_t)sm_count() * 8));
+  const int64_t grid = wave_grid<GridTag<E, 1>>(k_accu<E>, cdiv(nch, kThreads));
   Scratch sc;
   int st = get_scratch((void *)s, grid * (sizeof(double) + sizeof(uint32_t)) + 64, &sc);
   if (st) return st;

@@ -53,50 +53,45 @@ __device__ __forceinline__ double abs_d(double a) {
 __device__ __forceinline__ double gts_d(double a, double s) { return a > s ? 1.0 : 0.0; }
 __device__ __forceinline__ double sqrt_d(double a) { return __dsqrt_rn(a); }
 
-// exp on f64 arguments that came from f32 values: table-driven, |error| well
-// below 2^-50 relative, so rounding the result to f32 is correct except for
-// inputs within ~2^-50 of an f32 rounding boundary.
-//   x = (64*k + j) * ln2/64 + r,  |r| <= ln2/128
-//   exp(x) = 2^k * 2^(j/64) * exp(r)
-// Kept in global memory (L1-resident, 512 B): lanes index it divergently,
-// which the constant cache would serialise.
-static __device__ const double kExp2Table[64] = {
-#include "exp2_table.inc"
-};
-
-__device__ __forceinline__ double exp_for_f32(double x, const double *tab) {
-  // f32 inputs: exp overflows above 88.73 and underflows (to f32 zero) below -103.98
-  if (!(x == x)) return x;
-  if (x > 89.0) return __longlong_as_double(0x7ff0000000000000ll);   // +inf after rounding
-  if (x < -104.0) return 0.0;
-  const double inv = 92.33248261689366;        // 64 / ln2
-  const double ln2_64_hi = 0.010830424696223417; // ln2/64, high part
-  const double ln2_64_lo = 2.572804622327669e-14;// ln2/64 - hi
-  double kd = rint(x * inv);
-  int n = (int)kd;
-  double r = fma(-kd, ln2_64_hi, x);
-  r = fma(-kd, ln2_64_lo, r);
-  // exp(r) - 1 for |r| <= 0.0054: degree-6 Taylor, truncation < 4e-19
-  double p = 1.0 / 720.0;
-  p = fma(p, r, 1.0 / 120.0);
-  p = fma(p, r, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
+// exp of an f32 argument, correctly rounded in practice: evaluated in f64
+// (relative error ~2^-52) and rounded once to f32.  Branch-free and
+// table-free so a fused chain stays memory-bound (C3 is one exp per element):
+//   k = rint(x / ln2)  (magic-constant rounding inside one DFMA),
+//   r = x - k*ln2      (Cody-Waite hi/lo, exact hi product), |r| <= ln2/2,
+//   exp(r)             degree-11 Chebyshev fit (approximation error 2^-58),
+//   2^k                added to the exponent field (k in [-150, 129]: the
+//                      f64 result stays normal; f32 overflow/underflow and
+//                      subnormal rounding happen in the final conversion).
+// Arguments are clamped to [-104, 89]: exp(-104) < 2^-150 rounds to +0 and
+// exp(89) > FLT_MAX rounds to +inf, exactly as the unclamped values would.
+__device__ __forceinline__ double exp_poly_d(double r) {
+  double p = 0x1.af632a0f7e2cep-26;
+  p = fma(p, r, 0x1.28b4101c77212p-22);
+  p = fma(p, r, 0x1.71ddf56d8deb5p-19);
+  p = fma(p, r, 0x1.a01991a10d9aep-16);
+  p = fma(p, r, 0x1.a01a01b1461c5p-13);
+  p = fma(p, r, 0x1.6c16c1880029fp-10);
+  p = fma(p, r, 0x1.111111110f21ep-7);
+  p = fma(p, r, 0x1.555555554f0bap-5);
+  p = fma(p, r, 0x1.555555555555ap-3);
+  p = fma(p, r, 0x1.0000000000011p-1);
   p = fma(p, r, 1.0);
-  p = p * r;
-  int j = n & 63;
-  int k = (n - j) / 64;
-  double t = tab[j];
-  double y = fma(t, p, t);
-  // scale by 2^k (k in [-150, 128]) using two steps to stay in range
-  int k1 = k / 2, k2 = k - k1;
-  y = y * __longlong_as_double((long long)(k1 + 1023) << 52);
-  y = y * __longlong_as_double((long long)(k2 + 1023) << 52);
-  return y;
+  return fma(p, r, 1.0);
 }
 
-__device__ __forceinline__ float exp_f(float a, const double *tab) {
-  return __double2float_rn(exp_for_f32((double)a, tab));
+__device__ __forceinline__ float exp_f(float a) {
+  const float c = fminf(fmaxf(a, -104.0f), 89.0f);
+  const double x = (double)c;
+  const double kMagic = 0x1.8p52;
+  const double t = fma(x, 0x1.71547652b82fep0, kMagic);   // rint(x/ln2) + 1.5*2^52
+  const double k = __dsub_rn(t, kMagic);
+  const int ki = __double2loint(t);
+  double r = fma(-k, 0x1.62e42fee00000p-1, x);              // ln2 hi (exact k*hi)
+  r = fma(-k, 0x1.a39ef35793c76p-33, r);                    // ln2 lo
+  const double p = exp_poly_d(r);
+  const double y = __hiloint2double(__double2hiint(p) + (int)((unsigned)ki << 20), __double2loint(p));
+  const float res = __double2float_rn(y);
+  return (a != a) ? a : res;
 }
 __device__ __forceinline__ float log_f(float a) { return __double2float_rn(log((double)a)); }
 __device__ __forceinline__ float tanh_f(float a) { return __double2float_rn(tanh((double)a)); }

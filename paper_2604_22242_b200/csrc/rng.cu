@@ -63,6 +63,19 @@ __global__ void k_touch(uint4 *p, long long n16, unsigned salt) {
     p[i] = make_uint4(salt, (unsigned)i, salt ^ 0x5bd1e995u, (unsigned)(i >> 32));
 }
 
+// Read pass over the flush buffer: after k_touch evicted every input line,
+// reading the (now written-back) scratch leaves L2 holding only clean lines,
+// so the timed kernel neither hits its inputs in L2 nor pays for write-backs
+// of the flush's dirty lines.
+__global__ void k_read_sink(const uint4 *p, long long n16, unsigned *sink) {
+  unsigned acc = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x) {
+    uint4 w = __ldcg(p + i);
+    acc ^= w.x ^ w.y ^ w.z ^ w.w;
+  }
+  if (acc == 0x9e3779b9u && sink) *sink = acc;   // practically never taken; keeps the loads live
+}
+
 static unsigned grid_for(long long n, int threads) {
   long long g = (n + threads - 1) / threads;
   long long cap = (long long)sm_count() * 32;
@@ -127,6 +140,9 @@ int fm_flush_l2(void *scratch, size_t bytes, void *stream) {
   if (n16 == 0) return 0;
   k_touch<<<grid_for(n16, 512), 512, 0, (cudaStream_t)stream>>>((uint4 *)scratch, n16, salt++);
   FM_CHECK_LAUNCH("l2 flush kernel");
+  k_read_sink<<<grid_for(n16, 512), 512, 0, (cudaStream_t)stream>>>((const uint4 *)scratch, n16,
+                                                                    (unsigned *)scratch);
+  FM_CHECK_LAUNCH("l2 clean-read kernel");
   return 0;
 }
 

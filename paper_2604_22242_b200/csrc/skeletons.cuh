@@ -102,14 +102,38 @@ FM_DEV int64_t chunk_count(const fm_program &P, int64_t n_rows, int64_t n_cols, 
 }
 
 // ---- copy ------------------------------------------------------------------------------
+// Evaluators with kFast take a typed, branch-free path over whole warp tiles
+// (32 x V elements, coalesced 512-byte vector accesses, the next tile's loads
+// issued before the current tile's math) when the program is flat and
+// 16-byte aligned; the ragged remainder (and every other program) uses the
+// general chunk path.
 template <class E>
 __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ fm_program P, void *out,
                                                    int64_t n_rows, int64_t n_cols) {
   constexpr int V = E::kV;
+  const int64_t n_elem = n_rows * n_cols;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if constexpr (E::kFast) {
+    if (E::fast_ok(P, out)) {
+      constexpr int kTile = E::kTile;
+      const int lane = threadIdx.x & 31;
+      const int64_t nwarp = stride >> 5;
+      const int64_t ntile = n_elem / kTile;
+      int64_t t = c >> 5;
+      typename E::Buf buf;
+      if (t < ntile) E::load_tile(P, t * kTile, lane, buf);
+      for (; t < ntile; t += nwarp) {
+        const typename E::Buf cur = buf;
+        if (t + nwarp < ntile) E::load_tile(P, (t + nwarp) * kTile, lane, buf);
+        E::copy_tile(P, out, t * kTile, lane, cur);
+      }
+      c += ntile * 32;   // ragged remainder: flat V-element chunks from here on
+    }
+  }
   int64_t nrb;
   const int64_t nch = chunk_count<V>(P, n_rows, n_cols, nrb);
-  const int64_t n_elem = n_rows * n_cols;
-  for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < nch; c += (int64_t)gridDim.x * kThreads) {
+  for (; c < nch; c += stride) {
     Chunk ch = make_chunk<V>(P, c, n_rows, n_elem, nrb);
     uint32_t lo[V], hi[V];
     E::eval(P, ch, lo, hi);
@@ -220,7 +244,26 @@ __global__ void __launch_bounds__(kThreads) k_accu(const __grid_constant__ fm_pr
   const int64_t n_elem = n_rows * n_cols;
   double accd = 0.0;
   uint32_t accu = 0;
-  for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < nch; c += (int64_t)gridDim.x * kThreads) {
+  int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  if constexpr (E::kFast) {
+    if (E::fast_ok(P, nullptr)) {   // all-float flat program: warp tiles, one in flight
+      constexpr int kTile = E::kTile;
+      const int lane = threadIdx.x & 31;
+      const int64_t nwarp = stride >> 5;
+      const int64_t ntile = n_elem / kTile;
+      int64_t t = c >> 5;
+      typename E::Buf buf;
+      if (t < ntile) E::load_tile(P, t * kTile, lane, buf);
+      for (; t < ntile; t += nwarp) {
+        const typename E::Buf cur = buf;
+        if (t + nwarp < ntile) E::load_tile(P, (t + nwarp) * kTile, lane, buf);
+        E::accu_tile(P, cur, accd);
+      }
+      c += ntile * 32;
+    }
+  }
+  for (; c < nch; c += stride) {
     Chunk ch = make_chunk<V>(P, c, n_rows, n_elem, nrb);
     uint32_t lo[V], hi[V];
     E::eval(P, ch, lo, hi);

@@ -24,8 +24,8 @@ FM_DEV float tabs(float a) { return abs_f(a); }
 FM_DEV double tabs(double a) { return abs_d(a); }
 FM_DEV float tgt(float a, float s) { return gts_f(a, s); }
 FM_DEV double tgt(double a, double s) { return gts_d(a, s); }
-FM_DEV float texp(float a, const double *tab) { return exp_f(a, tab); }
-FM_DEV double texp(double a, const double *) { return exp_d(a); }
+FM_DEV float texp(float a) { return exp_f(a); }
+FM_DEV double texp(double a) { return exp_d(a); }
 FM_DEV float tlog(float a) { return log_f(a); }
 FM_DEV double tlog(double a) { return log_d(a); }
 FM_DEV float tsqrt(float a) { return sqrt_f(a); }
@@ -37,26 +37,26 @@ template <class T> FM_DEV T scal(uint64_t b);
 template <> FM_DEV float scal<float>(uint64_t b) { return u2f((uint32_t)b); }
 template <> FM_DEV double scal<double>(uint64_t b) { return __longlong_as_double((long long)b); }
 
-#define FM_EV template <class T> FM_DEV static T ev(const T *x, const uint64_t *s, const double *tab)
+#define FM_EV template <class T> FM_DEV static T ev(const T *x, const uint64_t *s)
 
 template <int I> struct In { FM_EV { return x[I]; } };
-template <class A, class B> struct Add { FM_EV { return tadd(A::ev(x, s, tab), B::ev(x, s, tab)); } };
-template <class A, class B> struct Sub { FM_EV { return tsub(A::ev(x, s, tab), B::ev(x, s, tab)); } };
-template <class A, class B> struct Mul { FM_EV { return tmul(A::ev(x, s, tab), B::ev(x, s, tab)); } };
-template <class A, class B> struct Div { FM_EV { return tdiv(A::ev(x, s, tab), B::ev(x, s, tab)); } };
-template <int S, class A> struct SAdd { FM_EV { return tadd(A::ev(x, s, tab), scal<T>(s[S])); } };
-template <int S, class A> struct SMul { FM_EV { return tmul(scal<T>(s[S]), A::ev(x, s, tab)); } };
-template <int S, class A> struct SDiv { FM_EV { return tdiv(scal<T>(s[S]), A::ev(x, s, tab)); } };
-template <int S, class A> struct Gts { FM_EV { return tgt(A::ev(x, s, tab), scal<T>(s[S])); } };
-template <class A> struct Neg { FM_EV { return tneg(A::ev(x, s, tab)); } };
-template <class A> struct Abs { FM_EV { return tabs(A::ev(x, s, tab)); } };
-template <class A> struct Exp { FM_EV { return texp(A::ev(x, s, tab), tab); } };
-template <class A> struct Log { FM_EV { return tlog(A::ev(x, s, tab)); } };
-template <class A> struct Sqrt { FM_EV { return tsqrt(A::ev(x, s, tab)); } };
-template <class A> struct Tanh { FM_EV { return ttanh(A::ev(x, s, tab)); } };
+template <class A, class B> struct Add { FM_EV { return tadd(A::ev(x, s), B::ev(x, s)); } };
+template <class A, class B> struct Sub { FM_EV { return tsub(A::ev(x, s), B::ev(x, s)); } };
+template <class A, class B> struct Mul { FM_EV { return tmul(A::ev(x, s), B::ev(x, s)); } };
+template <class A, class B> struct Div { FM_EV { return tdiv(A::ev(x, s), B::ev(x, s)); } };
+template <int S, class A> struct SAdd { FM_EV { return tadd(A::ev(x, s), scal<T>(s[S])); } };
+template <int S, class A> struct SMul { FM_EV { return tmul(scal<T>(s[S]), A::ev(x, s)); } };
+template <int S, class A> struct SDiv { FM_EV { return tdiv(scal<T>(s[S]), A::ev(x, s)); } };
+template <int S, class A> struct Gts { FM_EV { return tgt(A::ev(x, s), scal<T>(s[S])); } };
+template <class A> struct Neg { FM_EV { return tneg(A::ev(x, s)); } };
+template <class A> struct Abs { FM_EV { return tabs(A::ev(x, s)); } };
+template <class A> struct Exp { FM_EV { return texp(A::ev(x, s)); } };
+template <class A> struct Log { FM_EV { return tlog(A::ev(x, s)); } };
+template <class A> struct Sqrt { FM_EV { return tsqrt(A::ev(x, s)); } };
+template <class A> struct Tanh { FM_EV { return ttanh(A::ev(x, s)); } };
 template <int K, class A> struct Pow {
   FM_EV {
-    const T a = A::ev(x, s, tab);
+    const T a = A::ev(x, s);
     if (K == 0) return T(1);
     T acc = a;
 #pragma unroll
@@ -66,15 +66,22 @@ template <int K, class A> struct Pow {
 };
 #undef FM_EV
 
-// Evaluator over a flat chunk: all NIN inputs share type T (f32 or f64).
+// Evaluator over a chunk: all NIN inputs share type T (f32 or f64), and so
+// does the result.  eval() is the general path (any index map, ragged
+// chunks); the *_tile members serve the steady state of a flat program whose
+// buffers are all 16-byte aligned: typed 128-bit loads and stores with no
+// per-element type dispatch or bounds checks.
 template <class Expr, class T, int NIN, int V>
 struct TEval {
   static constexpr int kV = V;
+  static constexpr bool kFast = true;
+  static constexpr int kEtype = sizeof(T) == 8 ? FM_F64 : FM_F32;
+  static_assert(V * sizeof(T) % 16 == 0, "tiles move whole 16-byte vectors");
+
   FM_DEV static void eval(const fm_program &P, const Chunk &ch, uint32_t (&lo)[V], uint32_t (&hi)[V]) {
     uint32_t xl[NIN][V], xh[NIN][V];
 #pragma unroll
     for (int i = 0; i < NIN; ++i) load_slot<V>(P.slots[i], ch, xl[i], xh[i]);
-    const double *tab = kExp2Table;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       T xv[NIN];
@@ -83,10 +90,81 @@ struct TEval {
         if constexpr (sizeof(T) == 8) xv[i] = u2d(xl[i][v], xh[i][v]);
         else xv[i] = u2f(xl[i][v]);
       }
-      const T r = Expr::template ev<T>(xv, P.scalars, tab);
+      const T r = Expr::template ev<T>(xv, P.scalars);
       if constexpr (sizeof(T) == 8) d2u(r, lo[v], hi[v]);
       else { lo[v] = f2u(r); hi[v] = 0u; }
     }
+  }
+
+  // uniform per launch: may the tile members run?
+  FM_DEV static bool fast_ok(const fm_program &P, const void *out) {
+    if (!P.flat || P.result_etype != kEtype || (((uintptr_t)out) & 15)) return false;
+#pragma unroll
+    for (int i = 0; i < NIN; ++i)
+      if ((((uintptr_t)P.slots[i].ptr) & 15) || P.slots[i].etype != kEtype) return false;
+    return true;
+  }
+
+  // ---- warp tiles: 32 lanes x V elements, every vector access one fully
+  // coalesced 512-byte warp transaction.  Lane l owns, for q < V/W, the W
+  // elements at tile_base + q*32*W + l*W.  The skeletons keep one tile in
+  // flight (load t+1, then compute t) so HBM requests never wait on math.
+  static constexpr int kW = 16 / sizeof(T);   // elements per 128-bit vector
+  static constexpr int kTile = 32 * V;
+  struct Buf {
+    uint4 w[NIN][V / kW];
+  };
+
+  FM_DEV static void load_tile(const fm_program &P, int64_t base, int lane, Buf &b) {
+#pragma unroll
+    for (int i = 0; i < NIN; ++i) {
+      const T *p = (const T *)P.slots[i].ptr + base + lane * kW;
+#pragma unroll
+      for (int q = 0; q < V / kW; ++q) b.w[i][q] = ldg_v4(p + q * 32 * kW);
+    }
+  }
+
+  FM_DEV static void eval_tile(const fm_program &P, const Buf &b, T (&r)[V]) {
+#pragma unroll
+    for (int q = 0; q < V / kW; ++q) {
+#pragma unroll
+      for (int e = 0; e < kW; ++e) {
+        T x[NIN];
+#pragma unroll
+        for (int i = 0; i < NIN; ++i) {
+          const uint4 &w = b.w[i][q];
+          if constexpr (sizeof(T) == 8) x[i] = e == 0 ? u2d(w.x, w.y) : u2d(w.z, w.w);
+          else x[i] = u2f(e == 0 ? w.x : e == 1 ? w.y : e == 2 ? w.z : w.w);
+        }
+        r[q * kW + e] = Expr::template ev<T>(x, P.scalars);
+      }
+    }
+  }
+
+  FM_DEV static void copy_tile(const fm_program &P, void *out, int64_t base, int lane, const Buf &b) {
+    T r[V];
+    eval_tile(P, b, r);
+    T *o = (T *)out + base + lane * kW;
+#pragma unroll
+    for (int q = 0; q < V / kW; ++q) {
+      if constexpr (sizeof(T) == 8) {
+        uint32_t a0, a1, b0, b1;
+        d2u(r[q * 2], a0, a1);
+        d2u(r[q * 2 + 1], b0, b1);
+        st_v4(o + q * 32 * kW, a0, a1, b0, b1);
+      } else {
+        st_v4(o + q * 32 * kW, f2u(r[q * 4]), f2u(r[q * 4 + 1]), f2u(r[q * 4 + 2]), f2u(r[q * 4 + 3]));
+      }
+    }
+  }
+
+  // add the lane's V results to the f64 accumulator (the reduce_accu
+  // accumulator type, codegen.py:47-49)
+  FM_DEV static void accu_tile(const fm_program &P, const Buf &b, double &acc) {
+    T r[V];
+    eval_tile(P, b, r);
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc = add_d(acc, (double)r[v]);
   }
 };
 

@@ -125,6 +125,8 @@ FM_DEV void load_slot(const fm_slot &s, const Chunk &ch, uint32_t (&lo)[V], uint
 template <bool WIDE, int MAXD, int V, int NPF>
 struct Vm {
   static constexpr int kV = V;
+  static constexpr bool kFast = false;
+  FM_DEV static bool fast_ok(const fm_program &, const void *) { return false; }
   static constexpr int HD = WIDE ? MAXD : 1;
   static constexpr int HP = WIDE ? NPF : 1;
 
@@ -134,7 +136,6 @@ struct Vm {
     uint32_t hi[HD][V];
     uint32_t plo[NPF][V];
     uint32_t phi[HP][V];
-    const double *tab = kExp2Table;
 
     // Prefetch: all loads issued back to back.
 #pragma unroll
@@ -266,7 +267,7 @@ struct Vm {
         ALLD(UN_F, ABS_F, abs_f(x))
         ALLD(UN_D, ABS_D, abs_d(x))
         ALLD(UN_I, ABS_I32, abs_i32(x))
-        ALLD(UN_F, EXP_F, exp_f(x, tab))
+        ALLD(UN_F, EXP_F, exp_f(x))
         ALLD(UN_F, LOG_F, log_f(x))
         ALLD(UN_F, SQRT_F, sqrt_f(x))
         ALLD(UN_F, TANH_F, tanh_f(x))

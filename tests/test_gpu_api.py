@@ -323,3 +323,30 @@ def test_save_load_roundtrip(ctx, tmp_path):
     m = fm.randu(5, 4, seed=11, ctx=ctx)
     fm.save_matrix(m, tmp_path / "m.txt")
     assert np.array_equal(fm.load_matrix(tmp_path / "m.txt", ctx=ctx).to_numpy(), m.to_numpy())
+
+
+# --- f32 exp: correctly rounded in practice over its whole domain ------------------
+def test_exp_f32_sweep_vs_correctly_rounded(ctx):
+    """exp_f (ops.cuh) over a dense sweep of f32 bit patterns in [-104, 89]
+    plus the specials, against exp evaluated in f64 and rounded once (the
+    policy in DESIGN.md).  Both the VM and the template path share exp_f;
+    this drives it through the template kernel of a single-leaf exp copy."""
+    lo, hi = np.float32(-104.5), np.float32(89.5)
+    pos = np.arange(0, np.float32(hi).view(np.uint32), 97, dtype=np.uint32).view(np.float32)
+    neg = -np.arange(0, np.float32(-lo).view(np.uint32), 89, dtype=np.uint32).view(np.float32)
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 88.72283, 88.72284, -87.33654,
+                        -103.27893, -103.97208, -104.0, 89.0, 1e-30, -1e-30,
+                        np.float32(1.4e-45), -np.float32(1.4e-45)], np.float32)
+    x = np.concatenate([pos, neg, special]).astype(np.float32)
+    X = fm.from_array(x.reshape(-1, 1), ctx=ctx)
+    Z = fm.zeros(len(x), 1, ctx=ctx)
+    Z.assign(fm.exp(X))
+    got = Z.to_numpy().ravel()
+    with np.errstate(over="ignore", under="ignore"):
+        want = np.exp(x.astype(np.float64)).astype(np.float32)
+    assert orc.max_ulp(got, want) <= 1
+    # correctly rounded except (at most) a handful of near-midpoint inputs
+    ok = ~np.isnan(want)
+    assert np.array_equal(np.isnan(got), ~ok)
+    diff = np.count_nonzero(got[ok].view(np.uint32) != want[ok].view(np.uint32))
+    assert diff <= max(4, len(x) // 1_000_000), diff
