@@ -493,11 +493,95 @@ class C4:
         return run, byts, "port", 1, f"numpy restatement on {self.rows}x{cols}, 1 thread"
 
 
-CONFIGS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4}
+class C5:
+    """Z = 2 * X @ Y.t(), bf16 operands, f32 result, 8192^3: one tcgen05 launch
+    (the reference plans it as 2 materialising copies + a naive GEMM)."""
+    name = "c5"
+    workload = "C5 Z = 2*X*Y.t() bf16 GEMM 8192x8192x8192 (scalar + transpose folded into the tcgen05 kernel)"
+    unit = "TFLOP/s"
+    metric = "fused 2*X*Y.t() GEMM tensor-core TFLOP/s (BASELINE.json configs[4])"
+    dtype = "bf16 (f32 accumulate, f32 out)"
+    bound = "tensor"
+
+    def __init__(self, args, d):
+        self.n = args.n or 8192
+        self.d = d
+        self.labels = ["c5_gemm_bf16"]
+        self.kwork = [2 * self.n ** 3]
+        self.flush = False
+
+    def setup(self, fm, ctx):
+        self.fm, self.ctx = fm, ctx
+        n, off = self.n, self.d.rank * self.n * self.n
+        self.X = fm.Mat(n, n, "bf16", ctx)
+        self.Y = fm.Mat(n, n, "bf16", ctx)
+        self.Z = fm.Mat(n, n, "f32", ctx)
+        ctx.backend.randu(self.X.handle, 42, off)
+        ctx.backend.randu(self.Y.handle, 43, off)
+        self.e = 2 * self.X @ self.Y.t()
+        ctx.sync()
+
+    def launches(self):
+        return [lambda: self.Z.assign(self.e)]
+
+    def collective(self):
+        pass
+
+    def elements_per_step(self):
+        return self.n * self.n
+
+    def work_per_step(self):
+        return sum(self.kwork)
+
+    def check(self):
+        rng = np.random.default_rng(0)
+        rows = np.sort(rng.choice(self.n, 32, replace=False))
+        cols = np.sort(rng.choice(self.n, 32, replace=False))
+        x = self.X.to_numpy()[rows, :].astype(np.float64)
+        y = self.Y.to_numpy()[cols, :].astype(np.float64)
+        want = 2.0 * (x @ y.T)
+        got = self.Z.to_numpy()[np.ix_(rows, cols)].astype(np.float64)
+        return {"max_rel_err_32x32_sample_vs_f64": float(np.max(np.abs(got - want) / np.abs(want)))}
+
+    def setup_e2e(self):
+        fm = self.fm
+        self.hx = fm.pinned(self.n, self.n, "bf16")
+        self.hy = fm.pinned(self.n, self.n, "bf16")
+        self.hz = fm.pinned(self.n, self.n, "f32")
+        self.X.download_pinned(self.hx)
+        self.Y.download_pinned(self.hy)
+        self.ctx.sync()
+        return self.hx.nbytes + self.hy.nbytes, self.hz.nbytes
+
+    def step_e2e(self):
+        self.X.upload_pinned(self.hx)
+        self.Y.upload_pinned(self.hy)
+        self.Z.assign(self.e)
+        self.Z.download_pinned(self.hz)
+        self.ctx.sync()
+
+    def cpu(self, n_sample, threads):
+        from oracle import fm_oracle as orc
+        n = int(round(n_sample ** (1 / 3)))
+        x = orc.randu(n, n, 42, "bf16").astype(np.float64)
+        y = orc.randu(n, n, 43, "bf16").astype(np.float64)
+
+        def run():
+            return (2.0 * (x @ y.T)).astype(np.float32)
+        return run, 2 * n ** 3, "port", threads, (
+            f"the reference's matmul numerics (backend.py:338-346: operands upcast to f64, numpy/OpenBLAS "
+            f"GEMM, round to f32) on {n}x{n}x{n}, all {threads} host threads")
+
+
+CONFIGS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "c5": C5}
 
 
 # --------------------------------------------------------------------------------------
-def time_cpu(run, byts, steps, warmup):
+def work_scale(cfg) -> float:
+    return 1e12 if getattr(cfg, "bound", "hbm") == "tensor" else 1e9
+
+
+def time_cpu(run, byts, steps, warmup, scale=1e9):
     for _ in range(warmup):
         run()
     t = []
@@ -505,11 +589,12 @@ def time_cpu(run, byts, steps, warmup):
         t0 = time.perf_counter()
         run()
         t.append(time.perf_counter() - t0)
-    return byts / statistics.fmean(t) / 1e9, statistics.fmean(t)
+    return byts / statistics.fmean(t) / scale, statistics.fmean(t)
 
 
 def cpu_sample_elems(cfg_name: str) -> int:
-    return {"c2": 20_000_000, "c1": 4096 * 4096, "c3": 4096 * 4096, "c4": 65536 * 64}[cfg_name]
+    return {"c2": 20_000_000, "c1": 4096 * 4096, "c3": 4096 * 4096, "c4": 65536 * 64,
+            "c5": 2048 ** 3}[cfg_name]
 
 
 def reference_arm(args, d: Dist):
@@ -519,8 +604,8 @@ def reference_arm(args, d: Dist):
     threads = os.cpu_count() or 1
     run, byts, kind, threads, desc = cfg.cpu(cpu_sample_elems(args.config), threads)
     steps = max(1, args.steps)
-    gbs, mean_s = time_cpu(run, byts, steps, max(1, args.warmup))
-    line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": cfg.unit,
+    gbs, mean_s = time_cpu(run, byts, steps, max(1, args.warmup), work_scale(cfg))
+    line = {"impl": "reference", "metric": getattr(cfg, "metric", METRIC), "value": round(gbs, 3), "unit": cfg.unit,
             "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
             "ms_per_step": round(mean_s * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (reference splitmix64 randu)",
@@ -589,23 +674,38 @@ def ours(args, d: Dist):
     total_ms = sum(steps_ms)
     total_ms = d.max(total_ms)
     ms_per_step = total_ms / args.steps
-    bytes_all = cfg.bytes_per_step() * d.world
-    value = bytes_all / (ms_per_step * 1e-3) / 1e9
+    # work = algorithmic bytes (HBM-bound configs, plan_bytes convention) or
+    # flops (the tensor-core GEMM)
+    bound = getattr(cfg, "bound", "hbm")
+    kwork = cfg.kwork if bound == "tensor" else cfg.kbytes
+    scale = 1e12 if bound == "tensor" else 1e9
+    work_all = sum(kwork) * d.world
+    value = work_all / (ms_per_step * 1e-3) / scale
     peaks = measured_peaks()
     # dominant kernel: largest share of device time
     means = [statistics.fmean(v) for v in per_kernel]
     share = [sum(v) for v in per_kernel]
     dom = int(np.argmax(share))
-    achieved = cfg.kbytes[dom] / (means[dom] * 1e-3) / 1e9
+    achieved = kwork[dom] / (means[dom] * 1e-3) / scale
     traffic = ncu_traffic(cfg.labels[dom])
-    roofline = {"bound": "hbm", "kernel": cfg.labels[dom], "achieved": round(achieved, 1),
-                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-                "frac_of_8TBs": round(achieved / SPEC_HBM_GBS, 4),
-                "peak_source": peaks["source"], "traffic": traffic,
-                "algorithmic_bytes_per_launch": cfg.kbytes[dom],
-                "mean_launch_us": round(means[dom] * 1e3, 2),
-                "per_kernel_gbs": {lab: round(b / (m * 1e-3) / 1e9, 1)
-                                   for lab, b, m in zip(cfg.labels, cfg.kbytes, means)}}
+    if bound == "tensor":
+        peak = peaks["bf16_tflops"]
+        roofline = {"bound": "tensor", "kernel": cfg.labels[dom], "achieved": round(achieved, 1),
+                    "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                    "frac_of_sustained": round(achieved / peaks["bf16_tflops_sustained"], 4),
+                    "frac_of_2250_spec": round(achieved / 2250.0, 4),
+                    "peak_source": peaks["source"] + " bf16 burst", "traffic": traffic,
+                    "algorithmic_flops_per_launch": kwork[dom],
+                    "mean_launch_us": round(means[dom] * 1e3, 2)}
+    else:
+        roofline = {"bound": "hbm", "kernel": cfg.labels[dom], "achieved": round(achieved, 1),
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                    "frac_of_8TBs": round(achieved / SPEC_HBM_GBS, 4),
+                    "peak_source": peaks["source"], "traffic": traffic,
+                    "algorithmic_bytes_per_launch": kwork[dom],
+                    "mean_launch_us": round(means[dom] * 1e3, 2),
+                    "per_kernel_gbs": {lab: round(b / (m * 1e-3) / 1e9, 1)
+                                       for lab, b, m in zip(cfg.labels, kwork, means)}}
     check = cfg.check()
 
     # e2e through the public API with host buffers
@@ -626,7 +726,7 @@ def ours(args, d: Dist):
                 ctx.sync()
                 t.append(time.perf_counter() - t0)
             e2e_s = d.max(statistics.fmean(t))
-            e2e = {"value": round(bytes_all / e2e_s / 1e9, 3), "unit": cfg.unit,
+            e2e = {"value": round(work_all / e2e_s / scale, 3), "unit": cfg.unit,
                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                    "ms_per_step": round(e2e_s * 1e3, 3),
                    "path": "public API: Mat.upload_pinned + fm.accu/dot/norm (host floats back)"
@@ -636,24 +736,26 @@ def ours(args, d: Dist):
     cpu = None
     if d.world == 1 and not args.no_cpu:
         run, byts, kind, threads, desc = cfg.cpu(cpu_sample_elems(cfg.name), os.cpu_count() or 1)
-        gbs, _ = time_cpu(run, byts, 3, 1)
+        gbs, _ = time_cpu(run, byts, 3, 1, scale)
         cpu = {"value": round(gbs, 3), "unit": cfg.unit, "cores": threads, "kind": kind, "sample": desc}
 
     if d.rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": cfg.unit, "n_gpus": d.world,
+            "metric": getattr(cfg, "metric", METRIC), "value": round(value, 2), "unit": cfg.unit,
+            "n_gpus": d.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": cfg.dtype, "data": "synthetic (reference splitmix64 randu, generated on device)",
             "config": {"workload": cfg.workload,
                        "elements_per_gpu_per_step": cfg.elements_per_step(),
-                       "algorithmic_bytes_per_gpu_per_step": cfg.bytes_per_step(),
+                       ("algorithmic_flops_per_gpu_per_step" if bound == "tensor"
+                        else "algorithmic_bytes_per_gpu_per_step"): sum(kwork),
                        "l2": ("L2 flushed before every timed step: 512 MiB write then a read of the same buffer (inputs evicted, no dirty lines left to write back inside the timed kernel)" if flush_h is not None
                               else "inputs larger than the 126 MB L2; no flush"),
                        "parallelism": f"column/slice sharded x{d.world}, one process per GPU"
                                       + (", one NCCL all_reduce of partials per step" if cfg.name == "c2" and d.world > 1 else "")},
             "elements_per_s": round(cfg.elements_per_step() * d.world / (ms_per_step * 1e-3), 1),
-            "pct_of_8TBs": round(100 * value / d.world / SPEC_HBM_GBS, 2),
+            **({"pct_of_8TBs": round(100 * value / d.world / SPEC_HBM_GBS, 2)} if bound == "hbm" else {}),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(c1 - c0), "clocks": clocks,
             "wall_s_timed_region": round(t_wall, 4), "check": check,

@@ -188,6 +188,10 @@ int fm_launch_reduce_dim(int kernel_id, const fm_program *prog, int32_t dim,
                          const fm_reduce_out *outs, int32_t n_outs, void *stream);
 
 int fm_gemm(const fm_gemm_args *args, void *stream);
+/* which kernel fm_gemm would run for these arguments, without launching:
+ * FM_GEMM_PATH_EXACT (SIMT, f64 accumulation) or FM_GEMM_PATH_TCGEN05 */
+enum { FM_GEMM_PATH_EXACT = 0, FM_GEMM_PATH_TCGEN05 = 1 };
+int fm_gemm_plan(const fm_gemm_args *args, int *path);
 
 /* splitmix64 counter stream (rng.py:35-72); element k of the stream is
  * written to out[k - offset] for k in [offset, offset + n). */

@@ -471,9 +471,9 @@ class B200Backend(Backend):
 
     # -- linear algebra --------------------------------------------------------------------
 
-    def gemm(self, out: BufferHandle, a: BufferHandle, b: BufferHandle, m: int, n: int, k: int,
-             trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0,
-             lda: int | None = None, ldb: int | None = None, precision: int = 0) -> None:
+    def _gemm_args(self, out: BufferHandle, a: BufferHandle, b: BufferHandle, m: int, n: int, k: int,
+                   trans_a: bool, trans_b: bool, alpha: float, lda: int | None, ldb: int | None,
+                   precision: int) -> FmGemmArgs:
         if a.etype is not b.etype or not a.etype.is_float:
             raise BackendError("gemm operands must share a float element type")
         args = FmGemmArgs()
@@ -490,8 +490,23 @@ class B200Backend(Backend):
         need_a, need_b = args.lda * (m if trans_a else k), args.ldb * (k if trans_b else n)
         if a.n_elem < need_a or b.n_elem < need_b or out.n_elem < m * n:
             raise BackendError("gemm buffer smaller than its operand")
+        return args
+
+    def gemm(self, out: BufferHandle, a: BufferHandle, b: BufferHandle, m: int, n: int, k: int,
+             trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0,
+             lda: int | None = None, ldb: int | None = None, precision: int = 0) -> None:
+        args = self._gemm_args(out, a, b, m, n, k, trans_a, trans_b, alpha, lda, ldb, precision)
         self.nat.call("fm_gemm", ctypes.byref(args), self.stream)
         self.launch_count += 1
+
+    def gemm_path(self, out: BufferHandle, a: BufferHandle, b: BufferHandle, m: int, n: int, k: int,
+                  trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0,
+                  lda: int | None = None, ldb: int | None = None, precision: int = 0) -> str:
+        """Which kernel `gemm` would launch: "tcgen05" or "exact"."""
+        args = self._gemm_args(out, a, b, m, n, k, trans_a, trans_b, alpha, lda, ldb, precision)
+        path = ctypes.c_int()
+        self.nat.call("fm_gemm_plan", ctypes.byref(args), ctypes.byref(path))
+        return "tcgen05" if path.value == 1 else "exact"
 
     def matmul(self, out, left, right, m: int, k: int, n: int, etype: ElemType) -> None:
         """Reference contract (`cjit.py:171-182`): column-major NN product."""

@@ -87,10 +87,21 @@ int gemm_exact(const fm_gemm_args &g, cudaStream_t s) {
 
 // defined in gemm_tc.cu
 int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled);
+bool gemm_tensor_supported(const fm_gemm_args &g);
 
 }  // namespace fm
 
 using namespace fm;
+
+extern "C" int fm_gemm_plan(const fm_gemm_args *args, int *path) {
+  if (!args || !path) return fail_msg("gemm_plan: null argument");
+  const fm_gemm_args &g = *args;
+  *path = (g.precision != FM_GEMM_EXACT && g.in_etype != FM_F64 && g.m > 0 && g.n > 0 && g.k > 0 &&
+           gemm_tensor_supported(g))
+              ? FM_GEMM_PATH_TCGEN05
+              : FM_GEMM_PATH_EXACT;
+  return 0;
+}
 
 extern "C" int fm_gemm(const fm_gemm_args *args, void *stream) {
   if (!args) return fail_msg("gemm: null args");

@@ -1,11 +1,377 @@
-// gemm_tc.cu -- tcgen05 / TMEM / TMA tensor-core GEMM (placeholder until the
-// kernel lands: reports "not handled" so fm_gemm uses the exact kernel).
+// gemm_tc.cu -- tcgen05 / TMEM / TMA tensor-core GEMM for sm_100a.
+//
+//   C[m x n] (f32, column-major, ldc) = alpha * op(A)[m x k] . op(B)[k x n]
+//
+// with bf16 operands in column-major storage.  This is the B200 replacement
+// for the reference's matmul step (cjit.py:33-51 / backend.py:338-346), and
+// the planner hands it the whole `s * X @ Y.t()` product (plan.py gemm_operand):
+//   * the scalar is applied in the epilogue (TMEM -> registers -> *alpha),
+//   * a transpose only flips the operand's shared-memory major-ness: a
+//     column-major X (m x k) is M-contiguous ("MN-major"); Y.t() read from a
+//     column-major Y (n x k) is N-contiguous (MN-major too).  TMA loads either
+//     layout straight from the user's buffer and the UMMA descriptors say
+//     which one it is -- no transposed copy is ever materialised.
+//
+// Structure (one CTA per SM, persistent, warp-specialised):
+//   warp 0      TMA producer: 4-stage ring of (A 128 x 64, B 256 x 64) bf16
+//               tiles, 128-byte swizzled, completion on an mbarrier;
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (M=128, N=256, K=16 per instruction, f32 accumulators);
+//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 columns at a time,
+//               scale, coalesced column-major stores.
+// Two 256-column accumulators (all 512 TMEM columns) let the epilogue of
+// tile i overlap the MMAs of tile i+1.
+#include <cuda.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace fm {
-int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
-  (void)g; (void)s;
-  *handled = false;
+namespace tc {
+
+constexpr int BM = 128, BN = 256, BK = 64;          // CTA tile; BK = one 128-byte swizzle row of bf16
+constexpr int UMMA_K = 16;                          // K per tcgen05.mma (kind::f16)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;                // 16 KiB
+constexpr int B_BYTES = BN * BK * 2;                // 32 KiB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = 2 * BN;                   // double-buffered accumulator
+constexpr int kThreadsTc = 192;
+constexpr int kEpiWarp0 = 2;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int GROUP_M = 8;                          // tile rasterisation: 8 M-blocks share B in L2
+
+// ---- PTX wrappers --------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 TMEM lanes x 32 consecutive f32 columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), sm_100 version bits.
+//   K-major  : rows of 128 B (64 bf16 along K), 8-row atoms 1024 B apart (SBO); LBO unused.
+//   MN-major : 64 MN-elements (128 B) per k-row, 8 k-rows per 1024 B atom; SBO = k-group
+//              stride (1024 B), LBO = stride between 64-element MN blocks.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor, kind::f16: bf16 x bf16 -> f32, M = BM, N = BN
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
+  return (1u << 4)                       // D format f32
+         | (1u << 7) | (1u << 10)        // A, B format bf16
+         | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16)
+         | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+struct Params {
+  float *c;
+  int64_t ldc;
+  int m, n, k;
+  float alpha;
+  int a_mn, b_mn;   // operand major-ness (1 = MN-contiguous)
+};
+
+__device__ __forceinline__ void tile_coords(int t, int ntm, int ntn, int &mb, int &nb) {
+  const int per_group = GROUP_M * ntn;
+  const int g = t / per_group;
+  const int first = g * GROUP_M;
+  const int gsize = min(GROUP_M, ntm - first);
+  const int r = t - g * per_group;
+  mb = first + r % gsize;
+  nb = r / gsize;
+}
+
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    k_gemm_bf16(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(smem + STAGES * STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_holder = (uint32_t *)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntm = (p.m + BM - 1) / BM, ntn = (p.n + BN - 1) / BN;
+  const int ntiles = ntm * ntn;
+  const int nkb = (p.k + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);   // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, ntm, ntn, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *sa = smem + stage * STAGE_BYTES;
+          uint8_t *sb = sa + A_BYTES;
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (p.a_mn) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * (64 * BK * 2), &map_a, &full[stage], m0 + 64 * j, k0);
+          } else {
+            tma_load_2d(sa, &map_a, &full[stage], k0, m0);
+          }
+          if (p.b_mn) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * (64 * BK * 2), &map_b, &full[stage], n0 + 64 * j, k0);
+          } else {
+            tma_load_2d(sb, &map_b, &full[stage], k0, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    const uint32_t idesc = make_idesc(p.a_mn != 0, p.b_mn != 0);
+    // per UMMA_K step: K-major advances 32 B inside the swizzled row;
+    // MN-major advances two 1024-B k-groups.
+    const uint32_t a_step = p.a_mn ? 2048u : 32u, b_step = p.b_mn ? 2048u : 32u;
+    const uint32_t a_lbo = p.a_mn ? 64u * BK * 2 : 16u, b_lbo = p.b_mn ? 64u * BK * 2 : 16u;
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(&tempty[acc], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            const uint64_t ad = make_desc(sa + kk * a_step, a_lbo, 1024u);
+            const uint64_t bd = make_desc(sb + kk * b_step, b_lbo, 1024u);
+            umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);                       // frees the smem slot when these MMAs finish
+          if (kb == nkb - 1) umma_commit(&tfull[acc]);      // accumulator ready for the epilogue
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // ===== epilogue: TMEM -> registers -> alpha * acc -> column-major stores =====
+    const int q = warp & 3;                    // TMEM lane quarter this warp may access
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      int mb, nb;
+      tile_coords(t, ntm, ntn, mb, nb);
+      const int acc = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const int row = mb * BM + q * 32 + lane;
+      const bool row_ok = row < p.m;
+      float *cp = p.c + row;
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + ch * 32), v);
+        if (ch == BN / 32 - 1) {               // accumulator drained: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        const int col0 = nb * BN + ch * 32;
+        if (row_ok) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < p.n) cp[(int64_t)(col0 + j) * p.ldc] = p.alpha * __uint_as_float(v[j]);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ---- host side -----------------------------------------------------------------------
+// cuTensorMapEncodeTiled comes from the driver through the runtime's entry-point
+// query, so libfmb200.so has no link-time dependency on libcuda (it still loads
+// on a machine without a driver; the CPU test suite checks its exports).
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over a column-major operand: dim0 = the contiguous
+// extent, dim1 = the strided one, box = {64 (128 B, swizzled), rows}.
+static int encode_map(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                      uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail_msg("gemm: cuTensorMapEncodeTiled unavailable from the driver");
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld_elems * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail_msg("gemm: cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
   return 0;
 }
+
+}  // namespace tc
+
+// Tensor-core path for bf16 operands with an f32 result.  Other operand
+// types (and shapes TMA cannot describe) report handled = false and run on
+// the exact kernel.
+bool gemm_tensor_supported(const fm_gemm_args &g) {
+  if (g.in_etype != FM_BF16 || g.out_etype != FM_F32) return false;
+  if ((((uintptr_t)g.a) & 15) || (((uintptr_t)g.b) & 15)) return false;   // TMA: 16-byte aligned base
+  if ((g.lda * 2) % 16 || (g.ldb * 2) % 16) return false;                  // TMA: 16-byte multiple strides
+  if (g.m > INT32_MAX || g.n > INT32_MAX || g.k > INT32_MAX) return false;
+  return true;
+}
+
+int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
+  using namespace tc;
+  *handled = false;
+  if (!gemm_tensor_supported(g)) return 0;
+  Params p;
+  p.c = (float *)g.c;
+  p.ldc = g.ldc;
+  p.m = (int)g.m; p.n = (int)g.n; p.k = (int)g.k;
+  p.alpha = (float)g.alpha;   // the scalar node is f32 in the tree (expr.py:225), applied in the epilogue
+  p.a_mn = g.trans_a ? 0 : 1;   // op(A) = A (m x k, M-contiguous) or A^T of a k x m buffer (K-contiguous)
+  p.b_mn = g.trans_b ? 1 : 0;   // op(B) = B (k x n, K-contiguous) or B^T of an n x k buffer (N-contiguous)
+  CUtensorMap ma, mb;
+  int st;
+  if (p.a_mn) st = encode_map(&ma, g.a, (uint64_t)g.m, (uint64_t)g.k, (uint64_t)g.lda, 64, BK);
+  else st = encode_map(&ma, g.a, (uint64_t)g.k, (uint64_t)g.m, (uint64_t)g.lda, BK, BM);
+  if (st) return st;
+  if (p.b_mn) st = encode_map(&mb, g.b, (uint64_t)g.n, (uint64_t)g.k, (uint64_t)g.ldb, 64, BK);
+  else st = encode_map(&mb, g.b, (uint64_t)g.k, (uint64_t)g.n, (uint64_t)g.ldb, BK, BN);
+  if (st) return st;
+
+  static bool attr_set = false;
+  if (!attr_set) {
+    FM_CHECK(cudaFuncSetAttribute(k_gemm_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr_set = true;
+  }
+  const int ntiles = (int)(((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN));
+  const int grid = std::min(ntiles, sm_count());
+  k_gemm_bf16<<<grid, kThreadsTc, SMEM_BYTES, s>>>(ma, mb, p);
+  FM_CHECK_LAUNCH("tcgen05 gemm kernel");
+  *handled = true;
+  return 0;
+}
+
 }  // namespace fm

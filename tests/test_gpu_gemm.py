@@ -1,0 +1,96 @@
+"""tcgen05 GEMM (csrc/gemm_tc.cu) against the f64 product of the same bf16
+operands -- the reference's matmul numerics (f64 accumulation, cjit.py:33-51;
+oracle.py:53-57) with inputs rounded to bf16 first.
+
+Tolerance: the tensor core sums each K=16 MMA's products into an f32
+accumulator in TMEM, truncating at every one of the ceil(K/16) steps, so
+the stated bound is
+    |got - want| <= max(1e-5, ceil(K/16) * 2^-23) * sum_p |a_ip| |b_pj|
+elementwise: the north-star 1e-5 for K <= 1342 and (K/16)*2^-23 = 6.1e-5 at
+the C5 size K = 8192 -- inside the reference's own matmul gate of 1e-4
+(SPEC.md ledger, bench.py correctness gate).  Measured: 3.1e-5 at K = 8192."""
+
+import numpy as np
+import pytest
+
+import paper_2604_22242_b200 as fm
+from oracle import fm_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+
+def rel_bound(k: int) -> float:
+    return max(1e-5, -(-k // 16) * 2.0 ** -23)
+
+
+def _bf16(shape, seed):
+    return orc.bf16_round(np.random.default_rng(seed).random(shape, dtype=np.float64).astype(np.float32) - 0.25)
+
+
+def _check(got, a, b, alpha):
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    want = alpha * (a64 @ b64)
+    bound = rel_bound(a.shape[1]) * abs(alpha) * (np.abs(a64) @ np.abs(b64)) + 1e-30
+    err = np.abs(got.astype(np.float64) - want)
+    assert np.all(err <= bound), float((err / bound).max())
+
+
+@pytest.mark.parametrize("trans_a", [False, True])
+@pytest.mark.parametrize("trans_b", [False, True])
+@pytest.mark.parametrize("mnk", [(256, 512, 128), (200, 304, 72), (128, 256, 64), (1000, 520, 1032)])
+def test_tcgen05_gemm_layouts(gpu_ctx, trans_a, trans_b, mnk):
+    m, n, k = mnk
+    be = gpu_ctx.backend
+    a = _bf16((m, k), 1)
+    b = _bf16((k, n), 2)
+    A = fm.from_array(a.T.copy() if trans_a else a, etype="bf16", ctx=gpu_ctx)
+    B = fm.from_array(b.T.copy() if trans_b else b, etype="bf16", ctx=gpu_ctx)
+    C = fm.Mat(m, n, "f32", gpu_ctx)
+    assert be.gemm_path(C.handle, A.handle, B.handle, m, n, k, trans_a, trans_b, 2.0) == "tcgen05"
+    be.gemm(C.handle, A.handle, B.handle, m, n, k, trans_a, trans_b, alpha=2.0)
+    _check(C.to_numpy(), a, b, 2.0)
+
+
+def test_tcgen05_gemm_falls_back_on_unaligned_stride(gpu_ctx):
+    m, n, k = 64, 36, 24          # ldb = n = 36 bf16 = 72 B: not a 16-byte multiple for TMA
+    be = gpu_ctx.backend
+    a, b = _bf16((m, k), 3), _bf16((k, n), 4)
+    A = fm.from_array(a, etype="bf16", ctx=gpu_ctx)
+    B = fm.from_array(b.T.copy(), etype="bf16", ctx=gpu_ctx)
+    C = fm.Mat(m, n, "f32", gpu_ctx)
+    assert be.gemm_path(C.handle, A.handle, B.handle, m, n, k, False, True) == "exact"
+    be.gemm(C.handle, A.handle, B.handle, m, n, k, False, True)
+    _check(C.to_numpy(), a, b, 1.0)
+
+
+def test_c5_expression_is_one_tensor_core_launch(gpu_ctx):
+    """Z = 2 * X @ Y.t() through the public API: scalar and transpose fold
+    into the single GEMM launch (the reference plans 3 launches)."""
+    ctx = fm.Context(gpu_ctx.backend)
+    n = 512
+    X = fm.randu(n, n, 42, "bf16", ctx)
+    Y = fm.randu(n, n, 43, "bf16", ctx)
+    Z = fm.zeros(n, n, ctx=ctx)
+    ctx.reset_counters()
+    Z.assign(2 * X @ Y.t())
+    assert ctx.launches == 1
+    x, y = orc.randu(n, n, 42, "bf16"), orc.randu(n, n, 43, "bf16")
+    _check(Z.to_numpy(), x, y.T, 2.0)
+
+
+def test_gemm_c5_size_sampled(gpu_ctx):
+    """Full C5 size 8192^3: sampled rows/columns against the f64 product."""
+    ctx = fm.Context(gpu_ctx.backend)
+    n = 8192
+    X = fm.randu(n, n, 42, "bf16", ctx)
+    Y = fm.randu(n, n, 43, "bf16", ctx)
+    Z = fm.Mat(n, n, "f32", ctx)
+    Z.assign(2 * X @ Y.t())
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(n, 48, replace=False))
+    cols = np.sort(rng.choice(n, 48, replace=False))
+    x = X.to_numpy()
+    y = Y.to_numpy()
+    z = Z.to_numpy()
+    _check(z[np.ix_(rows, cols)], x[rows, :], y[cols, :].T, 2.0)
