@@ -123,8 +123,14 @@ def allreduce_rowstats(sums=None, maxs=None, mins=None, group=None):
     import torch.distributed as dist
     if sums is not None:
         dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
-    if maxs is not None:
-        dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
-    if mins is not None:
-        dist.all_reduce(mins, op=dist.ReduceOp.MIN, group=group)
+    # NCCL / gloo MAX and MIN do not propagate NaN the way numpy's max/min
+    # (and the device kernels) do: carry a NaN count beside the extrema and
+    # restore NaN wherever any rank saw one.
+    for t, op in ((maxs, dist.ReduceOp.MAX), (mins, dist.ReduceOp.MIN)):
+        if t is None:
+            continue
+        nan = t.isnan().to(t.dtype)
+        dist.all_reduce(nan, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(t, op=op, group=group)
+        t[nan > 0] = float("nan")
     return sums, maxs, mins
