@@ -205,6 +205,13 @@ int fm_copy(void *dst, const void *src, size_t bytes, void *stream);
 /* write `bytes` of scratch to evict L2 between timed trials */
 int fm_flush_l2(void *scratch, size_t bytes, void *stream);
 
+/* CUDA graphs: capture the launches enqueued on `stream` between begin and
+ * end into a replayable graph (per-step host work -> one graph launch) */
+int fm_graph_begin(void *stream);
+int fm_graph_end(void *stream, void **graph, int64_t *kernels);
+int fm_graph_launch(void *graph, void *stream);
+int fm_graph_destroy(void *graph);
+
 /* number of kernels this library launched since load (for bench gpu_launches) */
 int64_t fm_launch_counter(void);
 

@@ -115,6 +115,10 @@ SIGNATURES = {
     "fm_fill": [_P, _I32, _I64, ctypes.c_uint64, _P],
     "fm_copy": [_P, _P, _SZ, _P],
     "fm_flush_l2": [_P, _SZ, _P],
+    "fm_graph_begin": [_P],
+    "fm_graph_end": [_P, ctypes.POINTER(_P), ctypes.POINTER(_I64)],
+    "fm_graph_launch": [_P, _P],
+    "fm_graph_destroy": [_P],
     "fm_launch_counter": [],
 }
 _RESTYPES = {"fm_last_error": ctypes.c_char_p, "fm_launch_counter": ctypes.c_int64}

@@ -1,0 +1,279 @@
+// bulk.cuh -- TMA-bulk-staged copy skeleton for compute-heavy fused chains.
+//
+// The register-tile copy path (k_copy fast path) keeps one warp tile in
+// flight per warp, so its memory parallelism is bounded by registers and
+// occupancy.  For chains whose per-element math is long (a transcendental,
+// e.g. C3's exp), the warps spend most of their time computing and the loads
+// in flight fall below what HBM3e needs (profiles/r01/ncu_c3_copy.txt:
+// long-scoreboard stalls, 77 % DRAM throughput).  This skeleton decouples the
+// two: one producer warp streams fixed-size chunks of every input into a
+// ring of shared-memory stages with `cp.async.bulk` (TMA bulk copies,
+// completion counted on an mbarrier), and the consumer warps evaluate the
+// expression out of shared memory and store the results with 128-bit
+// coalesced st.global.  Bytes in flight per SM = (stages-1) x chunk x inputs,
+// independent of the consumers' register use.
+//
+// Persistent: one CTA per SM, chunks assigned round-robin.  The ragged tail
+// (< one chunk) is evaluated by the consumers with the general chunk path.
+#pragma once
+#include "skeletons.cuh"
+
+namespace fm {
+namespace bulk {
+
+constexpr int kConsumerWarps = 16;
+constexpr int kBulkThreads = (kConsumerWarps + 1) * 32;
+constexpr int kChunkBytes = 16384;        // per input per stage
+constexpr int kSmemBudget = 192 * 1024;
+
+FM_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+FM_DEV void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+FM_DEV void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+FM_DEV void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+FM_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// global -> shared bulk copy (TMA, no tensor map), completion on `bar`;
+// evict-first: every input byte is read exactly once.
+FM_DEV void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+FM_DEV uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+template <class E>
+struct Geometry {
+  using T = typename E::Elem;
+  static constexpr int kNin = E::kNin;
+  static constexpr int kChunk = kChunkBytes / (int)sizeof(T);               // elements per chunk
+  static constexpr int kStagesRaw = kSmemBudget / (kChunkBytes * (kNin > 0 ? kNin : 1));
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : (kStagesRaw < 2 ? 2 : kStagesRaw);
+  static constexpr int kSmem = kStages * kNin * kChunkBytes + 2 * kStages * 8 + 128;
+  static constexpr int kW = 16 / (int)sizeof(T);                            // elements per vector
+  static constexpr int kVecPerThread = kChunk / kW / (kConsumerWarps * 32);
+  static_assert(kChunk % (kW * kConsumerWarps * 32) == 0, "chunk splits evenly over consumers");
+};
+
+// shared-memory ring: [stage][input] chunks, then full[S] / empty[S] mbarriers
+template <class E>
+struct Ring {
+  using G = Geometry<E>;
+  unsigned char *base;
+  uint64_t *full, *empty;
+  FM_DEV explicit Ring(unsigned char *smem) {
+    base = smem;
+    full = (uint64_t *)(smem + G::kStages * G::kNin * kChunkBytes);
+    empty = full + G::kStages;
+  }
+  FM_DEV const unsigned char *chunk(int s, int i) const { return base + (s * G::kNin + i) * kChunkBytes; }
+  FM_DEV void init() {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < G::kStages; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], kConsumerWarps);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  // producer: one elected lane streams chunks c = blockIdx.x + k*gridDim.x
+  FM_DEV void produce(const fm_program &P, int64_t nfull) {
+    using T = typename E::Elem;
+    constexpr int S = G::kStages;
+    const uint64_t pol = evict_first_policy();
+    int64_t k = 0;
+    for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++k) {
+      const int s = (int)(k % S);
+      if (k >= S) mbar_wait(&empty[s], (uint32_t)(((k / S) & 1) ^ 1));
+      mbar_expect_tx(&full[s], G::kNin * kChunkBytes);
+#pragma unroll
+      for (int i = 0; i < G::kNin; ++i)
+        bulk_g2s((void *)chunk(s, i), (const T *)P.slots[i].ptr + c * G::kChunk, kChunkBytes, &full[s], pol);
+    }
+  }
+  // consumer: evaluate the kVecPerThread x kW elements of this thread in chunk stage s
+  FM_DEV void eval(const fm_program &P, int s, int ctid, typename E::Elem (&r)[G::kVecPerThread][G::kW]) const {
+    using T = typename E::Elem;
+    constexpr int NIN = G::kNin;
+#pragma unroll
+    for (int j = 0; j < G::kVecPerThread; ++j) {
+      const int q = ctid + j * kConsumerWarps * 32;
+      uint4 w[NIN];
+#pragma unroll
+      for (int i = 0; i < NIN; ++i) w[i] = *(const uint4 *)(chunk(s, i) + q * 16);
+#pragma unroll
+      for (int e = 0; e < G::kW; ++e) {
+        T x[NIN];
+#pragma unroll
+        for (int i = 0; i < NIN; ++i) {
+          if constexpr (sizeof(T) == 8) x[i] = e == 0 ? u2d(w[i].x, w[i].y) : u2d(w[i].z, w[i].w);
+          else x[i] = u2f(e == 0 ? w[i].x : e == 1 ? w[i].y : e == 2 ? w[i].z : w[i].w);
+        }
+        r[j][e] = E::ev_elem(P, x);
+      }
+    }
+  }
+  FM_DEV void release(int s) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+  }
+};
+
+template <class E>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+    k_copy_bulk(const __grid_constant__ fm_program P, void *out, int64_t n_elem) {
+  using G = Geometry<E>;
+  using T = typename E::Elem;
+  constexpr int S = G::kStages, C = G::kChunk;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Ring<E> ring(smem_raw);
+  ring.init();
+  const int warp = threadIdx.x >> 5;
+  const int64_t nfull = n_elem / C;
+  if (warp == kConsumerWarps) {
+    if ((threadIdx.x & 31) == 0) ring.produce(P, nfull);
+    return;
+  }
+  const int ctid = threadIdx.x;   // 0 .. kConsumerWarps*32-1
+  int64_t k = 0;
+  for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++k) {
+    const int s = (int)(k % S);
+    mbar_wait(&ring.full[s], (uint32_t)((k / S) & 1));
+    T r[G::kVecPerThread][G::kW];
+    ring.eval(P, s, ctid, r);
+    ring.release(s);   // smem reads done: free the stage before the long-latency stores
+    T *o = (T *)out + c * C;
+#pragma unroll
+    for (int j = 0; j < G::kVecPerThread; ++j) {
+      const int q = ctid + j * kConsumerWarps * 32;
+      if constexpr (sizeof(T) == 8) {
+        uint32_t a0, a1, b0, b1;
+        d2u(r[j][0], a0, a1);
+        d2u(r[j][1], b0, b1);
+        st_v4(o + q * 2, a0, a1, b0, b1);
+      } else {
+        st_v4(o + q * 4, f2u(r[j][0]), f2u(r[j][1]), f2u(r[j][2]), f2u(r[j][3]));
+      }
+    }
+  }
+
+  // ---- ragged tail: fewer than one chunk, general path, block 0 only ----
+  if (blockIdx.x == 0) {
+    constexpr int V = E::kV;
+    const int64_t base = nfull * C;
+    for (int64_t e0 = base + (int64_t)ctid * V; e0 < n_elem; e0 += (int64_t)kConsumerWarps * 32 * V) {
+      Chunk ch;
+      ch.base = e0;
+      ch.cnt = (int)min((int64_t)V, n_elem - e0);
+      ch.row0 = 0; ch.col = 0; ch.flat = true;
+      uint32_t lo[V], hi[V];
+      E::eval(P, ch, lo, hi);
+      store_chunk<V>(out, P.result_etype, ch.base, ch.cnt, lo, hi);
+    }
+  }
+}
+
+
+// Fused full reduction over bulk-staged chunks: per-thread f64 accumulation
+// (the reduce_accu accumulator type, codegen.py:47-49), block tree, per-block
+// partial, last-block finish -- one launch, deterministic for a grid.
+template <class E>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+    k_accu_bulk(const __grid_constant__ fm_program P, void *out, int64_t n_elem, int finalize,
+                double *part_d, unsigned *counter) {
+  using G = Geometry<E>;
+  using T = typename E::Elem;
+  constexpr int S = G::kStages, C = G::kChunk;
+  constexpr int NW = kConsumerWarps;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double smd[NW];
+  __shared__ bool last;
+  Ring<E> ring(smem_raw);
+  ring.init();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nfull = n_elem / C;
+  double acc = 0.0;
+  if (warp == NW) {
+    if (lane == 0) ring.produce(P, nfull);
+  } else {
+    const int ctid = threadIdx.x;
+    int64_t k = 0;
+    for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++k) {
+      const int s = (int)(k % S);
+      mbar_wait(&ring.full[s], (uint32_t)((k / S) & 1));
+      T r[G::kVecPerThread][G::kW];
+      ring.eval(P, s, ctid, r);
+      ring.release(s);
+#pragma unroll
+      for (int j = 0; j < G::kVecPerThread; ++j)
+#pragma unroll
+        for (int e = 0; e < G::kW; ++e) acc = add_d(acc, (double)r[j][e]);
+    }
+    if (blockIdx.x == gridDim.x - 1) {   // ragged tail (< one chunk): general path
+      constexpr int V = E::kV;
+      for (int64_t e0 = nfull * C + (int64_t)ctid * V; e0 < n_elem; e0 += (int64_t)NW * 32 * V) {
+        Chunk ch;
+        ch.base = e0;
+        ch.cnt = (int)min((int64_t)V, n_elem - e0);
+        ch.row0 = 0; ch.col = 0; ch.flat = true;
+        uint32_t lo[V], hi[V];
+        E::eval(P, ch, lo, hi);
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          if (v < ch.cnt) acc = add_d(acc, as_double(P.result_etype, lo[v], hi[v]));
+      }
+    }
+  }
+  // block tree over the consumer warps (the producer contributes 0)
+  acc = warp_sum_d(acc);
+  __syncthreads();
+  if (lane == 0 && warp < NW) smd[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < NW; ++w) b = add_d(b, smd[w]);
+    part_d[blockIdx.x] = b;
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (warp == 0) {
+    double sd = 0.0;
+    for (int i = lane; i < (int)gridDim.x; i += 32) sd = add_d(sd, ((volatile double *)part_d)[i]);
+    sd = warp_sum_d(sd);
+    if (lane == 0) {
+      if (finalize == FM_FINAL_SQRT) sd = sqrt_d(sd);
+      *(double *)out = sd;
+      *counter = 0u;
+    }
+  }
+}
+
+}  // namespace bulk
+}  // namespace fm

@@ -4,7 +4,10 @@
 // are multiples of the SM count (148) capped where partial results must be
 // combined.
 #pragma once
+#include <cstdlib>
+
 #include "common.cuh"
+#include "bulk.cuh"
 #include "skeletons.cuh"
 
 namespace fm {
@@ -33,10 +36,60 @@ int64_t wave_grid(K kernel, int64_t work_blocks) {
 }
 template <class E, int Skel> struct GridTag {};
 
+// Streaming path choice for an eligible template (flat, 16-byte aligned):
+// TMA-bulk staging (bulk.cuh) once the working set is well beyond L2 --
+// measured on B200 (profiles/r01): a light 2R+1W chain at 32768^2 runs
+// 5.47 TB/s on register tiles vs 6.49 TB/s bulk-staged, while at 4096^2
+// (1.5x L2) register tiles win (7.06 vs 6.89 TB/s).  Chains with a
+// transcendental are issue-bound rather than latency-bound and stay on
+// register tiles (C3: 6.22 vs 6.18 TB/s).  FMB200_BULK=0 / 1 forces one path
+// for every eligible template (A/B measurements).
+inline int bulk_override() {
+  static int v = [] {
+    const char *e = getenv("FMB200_BULK");
+    return (e && *e) ? atoi(e) : -1;
+  }();
+  return v;
+}
+constexpr int64_t kBulkMinBytes = 512ll << 20;
+inline bool bulk_wanted(int64_t working_set_bytes, bool heavy) {
+  const int ov = bulk_override();
+  return ov >= 0 ? ov == 1 : (!heavy && working_set_bytes >= kBulkMinBytes);
+}
+
+template <class E>
+bool host_fast_ok(const fm_program &P, const void *out) {
+  if (!P.flat || P.result_etype != E::kEtype || (((uintptr_t)out) & 15)) return false;
+  for (int i = 0; i < P.n_slots; ++i)
+    if ((((uintptr_t)P.slots[i].ptr) & 15) || P.slots[i].etype != E::kEtype) return false;
+  return true;
+}
+
+template <class E>
+int run_copy_bulk(const fm_program &P, void *out, int64_t n_elem, cudaStream_t s) {
+  using G = bulk::Geometry<E>;
+  static bool attr = false;
+  if (!attr) {
+    FM_CHECK(cudaFuncSetAttribute(bulk::k_copy_bulk<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
+    attr = true;
+  }
+  const int64_t chunks = n_elem / G::kChunk;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, sm_count()));
+  bulk::k_copy_bulk<E><<<(unsigned)grid, bulk::kBulkThreads, G::kSmem, s>>>(P, out, n_elem);
+  FM_CHECK_LAUNCH("fused copy kernel (bulk)");
+  return 0;
+}
+
 template <class E>
 int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s) {
   constexpr int V = E::kV;
   if (n_rows == 0 || n_cols == 0) return 0;
+  if constexpr (E::kFast) {
+    const int64_t n = n_rows * n_cols;
+    if (bulk_wanted(n * (E::kNin + 1) * (int64_t)sizeof(typename E::Elem), E::kHeavy) && P.n_slots == E::kNin &&
+        host_fast_ok<E>(P, out) && n >= (int64_t)bulk::Geometry<E>::kChunk * sm_count())
+      return run_copy_bulk<E>(P, out, n, s);
+  }
   const int64_t nrb = cdiv(n_rows, V);
   const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;
   const int64_t grid = wave_grid<GridTag<E, 0>>(k_copy<E>, cdiv(nch, kThreads));
@@ -46,9 +99,34 @@ int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cud
 }
 
 template <class E>
+int run_accu_bulk(const fm_program &P, void *out, int64_t n_elem, int finalize, cudaStream_t s) {
+  using G = bulk::Geometry<E>;
+  static bool attr = false;
+  if (!attr) {
+    FM_CHECK(cudaFuncSetAttribute(bulk::k_accu_bulk<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
+    attr = true;
+  }
+  const int64_t chunks = n_elem / G::kChunk;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, sm_count()));
+  Scratch sc;
+  int st = get_scratch((void *)s, grid * sizeof(double) + 64, &sc);
+  if (st) return st;
+  bulk::k_accu_bulk<E><<<(unsigned)grid, bulk::kBulkThreads, G::kSmem, s>>>(P, out, n_elem, finalize,
+                                                                            (double *)sc.payload, sc.counters);
+  FM_CHECK_LAUNCH("fused accu kernel (bulk)");
+  return 0;
+}
+
+template <class E>
 int run_accu(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, int finalize,
              cudaStream_t s) {
   constexpr int V = E::kV;
+  if constexpr (E::kFast) {
+    const int64_t n = n_rows * n_cols;
+    if (bulk_wanted(n * E::kNin * (int64_t)sizeof(typename E::Elem), E::kHeavy) && P.n_slots == E::kNin &&
+        host_fast_ok<E>(P, nullptr) && n >= (int64_t)bulk::Geometry<E>::kChunk * sm_count())
+      return run_accu_bulk<E>(P, out, n, finalize, s);
+  }
   const int64_t nrb = cdiv(n_rows, V);
   const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;
   const int64_t grid = wave_grid<GridTag<E, 1>>(k_accu<E>, cdiv(nch, kThreads));
@@ -70,7 +148,8 @@ int run_reduce_dim(const fm_program &P, int dim, int64_t n_rows, int64_t n_cols,
     return 0;
   }
   if (dim == 0) {
-    const int64_t grid = std::min<int64_t>(n_cols, (int64_t)sm_count() * 8);
+    // one persistent wave; columns are the work units (C4: 16384 / 444)
+    const int64_t grid = wave_grid<GridTag<E, 2>>(k_reduce_cols<E>, n_cols);
     k_reduce_cols<E><<<(unsigned)grid, kThreads, 0, s>>>(P, R, n_rows, n_cols);
     FM_CHECK_LAUNCH("fused column-reduction kernel");
     return 0;

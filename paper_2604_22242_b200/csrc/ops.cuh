@@ -54,42 +54,56 @@ __device__ __forceinline__ double gts_d(double a, double s) { return a > s ? 1.0
 __device__ __forceinline__ double sqrt_d(double a) { return __dsqrt_rn(a); }
 
 // exp of an f32 argument, correctly rounded in practice: evaluated in f64
-// (relative error ~2^-52) and rounded once to f32.  Branch-free and
-// table-free so a fused chain stays memory-bound (C3 is one exp per element):
-//   k = rint(x / ln2)  (magic-constant rounding inside one DFMA),
-//   r = x - k*ln2      (Cody-Waite hi/lo, exact hi product), |r| <= ln2/2,
-//   exp(r)             degree-11 Chebyshev fit (approximation error 2^-58),
-//   2^k                added to the exponent field (k in [-150, 129]: the
-//                      f64 result stays normal; f32 overflow/underflow and
-//                      subnormal rounding happen in the final conversion).
+// (relative error ~2^-52) and rounded once to f32.  Branch-free, so a fused
+// chain stays memory-bound (C3 is one exp per element), and short: 10 FP64
+// operations per element (the previous table-free degree-11 form took 16 and
+// kept C3 issue-bound, profiles/r01/ncu_c3_copy.txt):
+//   n = rint(x * 64/ln2)   (magic-constant rounding inside one DFMA),
+//   r = x - n*ln2/64       (Cody-Waite hi/lo, exact hi product), |r| <= ln2/128,
+//   exp(r) - 1             degree-5 Taylor polynomial (truncation 2^-54.6),
+//   2^(j/64)               64-entry table of correctly rounded f64 values
+//                          (j = n mod 64; read through L1, 512 bytes),
+//   2^(n div 64)           added to the exponent field (in [-150, 129]: the
+//                          f64 result stays normal; f32 overflow/underflow and
+//                          subnormal rounding happen in the final conversion).
 // Arguments are clamped to [-104, 89]: exp(-104) < 2^-150 rounds to +0 and
 // exp(89) > FLT_MAX rounds to +inf, exactly as the unclamped values would.
-__device__ __forceinline__ double exp_poly_d(double r) {
-  double p = 0x1.af632a0f7e2cep-26;
-  p = fma(p, r, 0x1.28b4101c77212p-22);
-  p = fma(p, r, 0x1.71ddf56d8deb5p-19);
-  p = fma(p, r, 0x1.a01991a10d9aep-16);
-  p = fma(p, r, 0x1.a01a01b1461c5p-13);
-  p = fma(p, r, 0x1.6c16c1880029fp-10);
-  p = fma(p, r, 0x1.111111110f21ep-7);
-  p = fma(p, r, 0x1.555555554f0bap-5);
-  p = fma(p, r, 0x1.555555555555ap-3);
-  p = fma(p, r, 0x1.0000000000011p-1);
-  p = fma(p, r, 1.0);
-  return fma(p, r, 1.0);
-}
+static __device__ const double kExp2Tab64[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
+};
 
 __device__ __forceinline__ float exp_f(float a) {
   const float c = fminf(fmaxf(a, -104.0f), 89.0f);
   const double x = (double)c;
   const double kMagic = 0x1.8p52;
-  const double t = fma(x, 0x1.71547652b82fep0, kMagic);   // rint(x/ln2) + 1.5*2^52
-  const double k = __dsub_rn(t, kMagic);
-  const int ki = __double2loint(t);
-  double r = fma(-k, 0x1.62e42fee00000p-1, x);              // ln2 hi (exact k*hi)
-  r = fma(-k, 0x1.a39ef35793c76p-33, r);                    // ln2 lo
-  const double p = exp_poly_d(r);
-  const double y = __hiloint2double(__double2hiint(p) + (int)((unsigned)ki << 20), __double2loint(p));
+  const double t = fma(x, 0x1.71547652b82fep+6, kMagic);   // rint(x*64/ln2) + 1.5*2^52
+  const double n = __dsub_rn(t, kMagic);
+  const int ni = __double2loint(t);
+  double r = fma(-n, 0x1.62e42fee00000p-7, x);             // ln2/64 hi (exact n*hi)
+  r = fma(-n, 0x1.a39ef35793c76p-39, r);                   // ln2/64 lo
+  double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  const double p = __dmul_rn(q, r);                         // exp(r) - 1
+  const double tj = __ldg(&kExp2Tab64[ni & 63]);
+  const double y0 = fma(tj, p, tj);                         // 2^(j/64) * exp(r)
+  const double y = __hiloint2double(__double2hiint(y0) + (int)((unsigned)(ni >> 6) << 20), __double2loint(y0));
   const float res = __double2float_rn(y);
   return (a != a) ? a : res;
 }

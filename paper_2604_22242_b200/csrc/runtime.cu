@@ -5,6 +5,8 @@
 #include <mutex>
 #include <string>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace fm {
@@ -186,13 +188,74 @@ int fm_event_destroy(void *event) {
 }
 
 int fm_event_record(void *event, void *stream) {
-  FM_CHECK(cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream));
+  // Under stream capture a plain record is only a capture-internal
+  // dependency; an external record becomes an event-record node of the graph,
+  // so the event still times the replayed kernels.
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  FM_CHECK(cudaStreamIsCapturing((cudaStream_t)stream, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    FM_CHECK(cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream, cudaEventRecordExternal));
+  else
+    FM_CHECK(cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream));
   return 0;
 }
 
 int fm_event_elapsed_ms(void *start, void *stop, float *ms) {
   FM_CHECK(cudaEventSynchronize((cudaEvent_t)stop));
   FM_CHECK(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)stop));
+  return 0;
+}
+
+// ---- CUDA graphs: capture a sequence of launches on a stream, replay it ----
+// Replaces per-step host work (planning, binding, ctypes) with one
+// cudaGraphLaunch; the captured kernels are exactly the ones the eager calls
+// enqueue.  The launch counter advances by the graph's kernel count per replay.
+struct FmGraph {
+  cudaGraphExec_t exec;
+  int64_t kernels;
+};
+
+int fm_graph_begin(void *stream) {
+  FM_CHECK(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
+  return 0;
+}
+
+int fm_graph_end(void *stream, void **graph, int64_t *kernels) {
+  cudaGraph_t g;
+  FM_CHECK(cudaStreamEndCapture((cudaStream_t)stream, &g));
+  size_t n = 0;
+  cudaGraphGetNodes(g, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n) cudaGraphGetNodes(g, nodes.data(), &n);
+  int64_t k = 0;
+  for (size_t i = 0; i < n; ++i) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+  }
+  cudaGraphExec_t exec;
+  cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail("cudaGraphInstantiate", e);
+  FmGraph *fg = new FmGraph{exec, k};
+  *graph = fg;
+  if (kernels) *kernels = k;
+  return 0;
+}
+
+int fm_graph_launch(void *graph, void *stream) {
+  if (!graph) return fail_msg("graph_launch: null graph");
+  FmGraph *fg = (FmGraph *)graph;
+  FM_CHECK(cudaGraphLaunch(fg->exec, (cudaStream_t)stream));
+  count_launch(fg->kernels);
+  return 0;
+}
+
+int fm_graph_destroy(void *graph) {
+  if (!graph) return 0;
+  FmGraph *fg = (FmGraph *)graph;
+  cudaError_t e = cudaGraphExecDestroy(fg->exec);
+  delete fg;
+  if (e != cudaSuccess) return fail("cudaGraphExecDestroy", e);
   return 0;
 }
 

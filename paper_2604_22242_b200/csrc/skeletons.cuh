@@ -10,6 +10,8 @@
 // returning the result bits of V consecutive elements (the root's element
 // type is P.result_etype).
 #pragma once
+#include <math_constants.h>
+
 #include "vm.cuh"
 
 namespace fm {
@@ -381,9 +383,49 @@ FM_DEV unsigned needed_stats(const ReduceOuts &R) {
   return need;
 }
 
-// dim 0: one block per column (grid-stride over columns)
+// Typed per-thread column statistics for the fast path.  A thread visits its
+// rows in strictly increasing order, so "first index wins" needs no index
+// compare: a later element replaces the candidate only if strictly better,
+// or if it is the first NaN (numpy semantics), or if there is no candidate
+// yet.  Branch-free selects; 32-bit row indices (outputs are u32).
+template <class T>
+struct ColStats {
+  static constexpr uint32_t kNone = 0xFFFFFFFFu;
+  double sum;
+  T mx, mn;
+  uint32_t imx, imn;
+  FM_DEV void init() {
+    sum = 0.0;
+    mx = -CUDART_INF_F; mn = CUDART_INF_F;   // converts exactly for T = double
+    imx = imn = kNone;
+  }
+  FM_DEV void add(T x, uint32_t i, unsigned need) {
+    if (need & 1u) sum = add_d(sum, (double)x);
+    if (need & 2u) {
+      const bool take = (!(x <= mx) || imx == kNone) && (mx == mx);
+      mx = take ? x : mx;
+      imx = take ? i : imx;
+    }
+    if (need & 4u) {
+      const bool take = (!(x >= mn) || imn == kNone) && (mn == mn);
+      mn = take ? x : mn;
+      imn = take ? i : imn;
+    }
+  }
+  FM_DEV void to_stats(Stats &s) const {
+    s.sum += sum;
+    if (imx != kNone) { s.mx.v = (double)mx; s.mx.i = imx; }
+    if (imn != kNone) { s.mn.v = (double)mn; s.mn.i = imn; }
+  }
+};
+
+// dim 0: one block per column (grid-stride over columns).  Fast path (typed
+// evaluator, flat program, 16-byte aligned columns): each warp streams warp
+// tiles of its column with the next tile's loads in flight while the current
+// tile's statistics are folded in; ragged row remainders and every other
+// program use the general chunk path.
 template <class E>
-__global__ void __launch_bounds__(kThreads) k_reduce_cols(const __grid_constant__ fm_program P,
+__global__ void __launch_bounds__(kThreads, 3) k_reduce_cols(const __grid_constant__ fm_program P,
                                                           const __grid_constant__ ReduceOuts R,
                                                           int64_t n_rows, int64_t n_cols) {
   constexpr int V = E::kV;
@@ -393,10 +435,45 @@ __global__ void __launch_bounds__(kThreads) k_reduce_cols(const __grid_constant_
   const int rt = P.result_etype;
   const bool fl = is_float_etype(rt);
   const unsigned need = needed_stats(R);
+  bool fast = false;
+  int64_t fast_rows = 0;
+  if constexpr (E::kFast) {
+    using T = typename E::Elem;
+    fast = E::fast_ok(P, nullptr) && ((n_rows * (int64_t)sizeof(T)) & 15) == 0 && n_rows < 0xFFFFFFFFll;
+    if (fast) fast_rows = (n_rows / E::kTile) * E::kTile;
+  }
   for (int64_t col = blockIdx.x; col < n_cols; col += gridDim.x) {
     Stats s;
     stats_init(s);
-    for (int64_t row0 = (int64_t)threadIdx.x * V; row0 < n_rows; row0 += (int64_t)kThreads * V) {
+    int64_t row_start = 0;
+    if constexpr (E::kFast) {
+      if (fast) {
+        using T = typename E::Elem;
+        constexpr int kTile = E::kTile, kW = E::kW;
+        const int lane = threadIdx.x & 31;
+        const int64_t ntile = fast_rows / kTile;
+        const int64_t cbase = col * n_rows;
+        ColStats<T> cs;
+        cs.init();
+        int64_t t = threadIdx.x >> 5;
+        typename E::Buf buf;
+        if (t < ntile) E::load_tile(P, cbase + t * kTile, lane, buf);
+        for (; t < ntile; t += kThreads / 32) {
+          const typename E::Buf cur = buf;
+          if (t + kThreads / 32 < ntile) E::load_tile(P, cbase + (t + kThreads / 32) * kTile, lane, buf);
+          T r[V];
+          E::eval_tile(P, cur, r);
+          const uint32_t r0 = (uint32_t)(t * kTile) + lane * kW;
+#pragma unroll
+          for (int q = 0; q < V / kW; ++q)
+#pragma unroll
+            for (int e = 0; e < kW; ++e) cs.add(r[q * kW + e], r0 + q * 32 * kW + e, need);
+        }
+        cs.to_stats(s);
+        row_start = fast_rows;
+      }
+    }
+    for (int64_t row0 = row_start + (int64_t)threadIdx.x * V; row0 < n_rows; row0 += (int64_t)kThreads * V) {
       Chunk ch;
       ch.row0 = row0; ch.col = col; ch.base = row0 + col * n_rows;
       ch.cnt = (int)min((int64_t)V, n_rows - row0);

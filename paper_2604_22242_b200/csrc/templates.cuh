@@ -66,6 +66,26 @@ template <int K, class A> struct Pow {
 };
 #undef FM_EV
 
+// Heavy<Expr>::v -- the chain contains a transcendental: its per-element math
+// is long enough that the copy skeleton should stage inputs through shared
+// memory with TMA bulk copies (bulk.cuh) instead of register tiles.
+template <class X> struct Heavy { static constexpr bool v = false; };
+template <class A> struct Heavy<Exp<A>> { static constexpr bool v = true; };
+template <class A> struct Heavy<Log<A>> { static constexpr bool v = true; };
+template <class A> struct Heavy<Tanh<A>> { static constexpr bool v = true; };
+template <class A> struct Heavy<Neg<A>> { static constexpr bool v = Heavy<A>::v; };
+template <class A> struct Heavy<Abs<A>> { static constexpr bool v = Heavy<A>::v; };
+template <class A> struct Heavy<Sqrt<A>> { static constexpr bool v = Heavy<A>::v; };
+template <int K, class A> struct Heavy<Pow<K, A>> { static constexpr bool v = Heavy<A>::v; };
+template <int S, class A> struct Heavy<SAdd<S, A>> { static constexpr bool v = Heavy<A>::v; };
+template <int S, class A> struct Heavy<SMul<S, A>> { static constexpr bool v = Heavy<A>::v; };
+template <int S, class A> struct Heavy<SDiv<S, A>> { static constexpr bool v = Heavy<A>::v; };
+template <int S, class A> struct Heavy<Gts<S, A>> { static constexpr bool v = Heavy<A>::v; };
+template <class A, class B> struct Heavy<Add<A, B>> { static constexpr bool v = Heavy<A>::v || Heavy<B>::v; };
+template <class A, class B> struct Heavy<Sub<A, B>> { static constexpr bool v = Heavy<A>::v || Heavy<B>::v; };
+template <class A, class B> struct Heavy<Mul<A, B>> { static constexpr bool v = Heavy<A>::v || Heavy<B>::v; };
+template <class A, class B> struct Heavy<Div<A, B>> { static constexpr bool v = Heavy<A>::v || Heavy<B>::v; };
+
 // Evaluator over a chunk: all NIN inputs share type T (f32 or f64), and so
 // does the result.  eval() is the general path (any index map, ragged
 // chunks); the *_tile members serve the steady state of a flat program whose
@@ -73,8 +93,15 @@ template <int K, class A> struct Pow {
 // per-element type dispatch or bounds checks.
 template <class Expr, class T, int NIN, int V>
 struct TEval {
+  using Elem = T;
   static constexpr int kV = V;
+  static constexpr int kNin = NIN;
   static constexpr bool kFast = true;
+  static constexpr bool kHeavy = Heavy<Expr>::v;
+
+  FM_DEV static T ev_elem(const fm_program &P, const T (&x)[NIN]) {
+    return Expr::template ev<T>(x, P.scalars);
+  }
   static constexpr int kEtype = sizeof(T) == 8 ? FM_F64 : FM_F32;
   static_assert(V * sizeof(T) % 16 == 0, "tiles move whole 16-byte vectors");
 

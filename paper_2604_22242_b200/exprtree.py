@@ -59,6 +59,8 @@ class ElemType(enum.Enum):
     def of(cls, value: "ElemType | str") -> "ElemType":
         if isinstance(value, cls):
             return value
+        if not isinstance(value, str) and isinstance(getattr(value, "value", None), str):
+            value = value.value     # a foreign enum with the same values (fusemat.expr.ElemType)
         try:
             return cls(value)
         except ValueError:

@@ -350,3 +350,36 @@ def test_exp_f32_sweep_vs_correctly_rounded(ctx):
     assert np.array_equal(np.isnan(got), ~ok)
     diff = np.count_nonzero(got[ok].view(np.uint32) != want[ok].view(np.uint32))
     assert diff <= max(4, len(x) // 1_000_000), diff
+
+
+# --- CUDA graph capture / replay --------------------------------------------------
+def test_graph_capture_replays_the_same_kernels(ctx):
+    """fm.capture records the launches of a step; replay re-runs them on the
+    current buffer contents (one cudaGraphLaunch)."""
+    from paper_2604_22242_b200._native import native
+    n = 1 << 20
+    x = fm.randu(n, 1, 11, "f32", ctx)
+    y = fm.randu(n, 1, 12, "f32", ctx)
+    z = fm.zeros(n, 1, ctx=ctx)
+    r = fm.Mat(2, 1, "f64", ctx)
+
+    def step():
+        z.assign(2 * (x % y) + x)
+        fm.dot_async(x, y, r, 0)
+        fm.norm_async(x - y, r, 1)
+
+    g = fm.capture(step, ctx)
+    assert g.kernels == 3
+    c0 = native().lib.fm_launch_counter()
+    g.replay()
+    assert native().lib.fm_launch_counter() - c0 == 3
+    xv, yv = x.to_numpy(), y.to_numpy()
+    assert orc.max_ulp(z.to_numpy(), np.float32(2) * (xv * yv) + xv) == 0
+    got = r.to_numpy().ravel()
+    want_dot = orc.accu(xv * yv, orc.ElemType.f32)
+    assert abs(got[0] - want_dot) <= 1e-12 * abs(want_dot)
+    # new inputs, same graph: results follow the buffers
+    x.set_values(yv.reshape(-1, 1))
+    g.replay()
+    assert orc.max_ulp(z.to_numpy(), np.float32(2) * (yv * yv) + yv) == 0
+    g.close()
