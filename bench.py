@@ -573,7 +573,55 @@ class C5:
             f"GEMM, round to f32) on {n}x{n}x{n}, all {threads} host threads")
 
 
-CONFIGS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "c5": C5}
+class C5F32(C5):
+    """Z = 2 * X @ Y.t() with f32 operands: each operand split into three bf16
+    planes and the six significant plane products accumulated by the same
+    tcgen05 kernel (3 launches: two splits + the GEMM).  TFLOP/s counts the
+    2*N^3 of the f32 product, not the 6x tensor-core work."""
+    name = "c5f32"
+    workload = "C5 Z = 2*X*Y.t() f32 GEMM 8192x8192x8192 (split-bf16 x6 on tcgen05; scalar + transpose folded)"
+    metric = "fused 2*X*Y.t() GEMM TFLOP/s (BASELINE.json configs[4], f32 operands)"
+    dtype = "f32 operands (3 bf16 planes each, f32 accumulate, f32 out)"
+
+    def __init__(self, args, d):
+        super().__init__(args, d)
+        self.labels = ["c5_gemm_f32"]
+
+    def setup(self, fm, ctx):
+        self.fm, self.ctx = fm, ctx
+        n, off = self.n, self.d.rank * self.n * self.n
+        self.X = fm.Mat(n, n, "f32", ctx)
+        self.Y = fm.Mat(n, n, "f32", ctx)
+        self.Z = fm.Mat(n, n, "f32", ctx)
+        ctx.backend.randu(self.X.handle, 42, off)
+        ctx.backend.randu(self.Y.handle, 43, off)
+        self.e = 2 * self.X @ self.Y.t()
+        ctx.sync()
+
+    def setup_e2e(self):
+        fm = self.fm
+        self.hx = fm.pinned(self.n, self.n, "f32")
+        self.hy = fm.pinned(self.n, self.n, "f32")
+        self.hz = fm.pinned(self.n, self.n, "f32")
+        self.X.download_pinned(self.hx)
+        self.Y.download_pinned(self.hy)
+        self.ctx.sync()
+        return self.hx.nbytes + self.hy.nbytes, self.hz.nbytes
+
+    def cpu(self, n_sample, threads):
+        from oracle import fm_oracle as orc
+        n = int(round(n_sample ** (1 / 3)))
+        x = orc.randu(n, n, 42, "f32").astype(np.float64)
+        y = orc.randu(n, n, 43, "f32").astype(np.float64)
+
+        def run():
+            return (2.0 * (x @ y.T)).astype(np.float32)
+        return run, 2 * n ** 3, "port", threads, (
+            f"the reference's matmul numerics (backend.py:338-346: f32 operands upcast to f64, numpy/OpenBLAS "
+            f"GEMM, round to f32) on {n}x{n}x{n}, all {threads} host threads")
+
+
+CONFIGS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "c5": C5, "c5f32": C5F32}
 
 
 # --------------------------------------------------------------------------------------
@@ -594,7 +642,7 @@ def time_cpu(run, byts, steps, warmup, scale=1e9):
 
 def cpu_sample_elems(cfg_name: str) -> int:
     return {"c2": 20_000_000, "c1": 4096 * 4096, "c3": 4096 * 4096, "c4": 65536 * 64,
-            "c5": 2048 ** 3}[cfg_name]
+            "c5": 2048 ** 3, "c5f32": 2048 ** 3}[cfg_name]
 
 
 def reference_arm(args, d: Dist):

@@ -136,7 +136,8 @@ typedef struct {
 } fm_gemm_args;
 
 enum {
-  FM_GEMM_AUTO = 0,     /* bf16 -> tensor core; f32 -> split-bf16 tensor core; f64 -> SIMT */
+  FM_GEMM_AUTO = 0,     /* bf16 -> tensor core; f32 -> split-bf16 tensor core when m*n*k >= 2^28,
+                           else SIMT exact; f64 -> SIMT */
   FM_GEMM_TENSOR = 1,   /* force tcgen05 path (bf16, f32 via 3-way bf16 split) */
   FM_GEMM_EXACT = 2     /* SIMT, f64 accumulation (reference cjit.py:33-51 numerics) */
 };

@@ -93,13 +93,21 @@ bool gemm_tensor_supported(const fm_gemm_args &g);
 
 using namespace fm;
 
+// FM_GEMM_AUTO: bf16 always on the tensor cores (exact products, ~1e-6);
+// f32 on the split-bf16 tensor path only when the product is big enough to
+// pay for the operand splits -- small f32 GEMMs keep the reference's exact
+// f64-accumulated numerics bit for bit (cjit.py:33-51) at no cost.
+static bool use_tensor(const fm_gemm_args &g) {
+  if (g.precision == FM_GEMM_EXACT || g.in_etype == FM_F64) return false;
+  if (g.m <= 0 || g.n <= 0 || g.k <= 0 || !gemm_tensor_supported(g)) return false;
+  if (g.precision == FM_GEMM_AUTO && g.in_etype == FM_F32 && (double)g.m * g.n * g.k < (double)(1ll << 28))
+    return false;
+  return true;
+}
+
 extern "C" int fm_gemm_plan(const fm_gemm_args *args, int *path) {
   if (!args || !path) return fail_msg("gemm_plan: null argument");
-  const fm_gemm_args &g = *args;
-  *path = (g.precision != FM_GEMM_EXACT && g.in_etype != FM_F64 && g.m > 0 && g.n > 0 && g.k > 0 &&
-           gemm_tensor_supported(g))
-              ? FM_GEMM_PATH_TCGEN05
-              : FM_GEMM_PATH_EXACT;
+  *path = use_tensor(*args) ? FM_GEMM_PATH_TCGEN05 : FM_GEMM_PATH_EXACT;
   return 0;
 }
 
@@ -118,7 +126,7 @@ extern "C" int fm_gemm(const fm_gemm_args *args, void *stream) {
     for (int64_t j = 0; j < g.n; ++j) FM_CHECK(cudaMemsetAsync((char *)g.c + j * g.ldc * w, 0, g.m * w, s));
     return 0;
   }
-  if (g.precision != FM_GEMM_EXACT && g.in_etype != FM_F64) {
+  if (use_tensor(g)) {
     bool handled = false;
     int st = gemm_tensor(g, s, &handled);
     if (st || handled) return st;

@@ -22,8 +22,10 @@
 // Two 256-column accumulators (all 512 TMEM columns) let the epilogue of
 // tile i overlap the MMAs of tile i+1.
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -37,8 +39,17 @@ constexpr int A_BYTES = BM * BK * 2;                // 16 KiB
 constexpr int B_BYTES = BN * BK * 2;                // 32 KiB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 2 * BN;                   // double-buffered accumulator
-constexpr int kThreadsTc = 192;
-constexpr int kEpiWarp0 = 2;
+// 2 per TMEM lane quarter, 128 columns each.  10 warps put 3 on some SM
+// sub-partition (16K registers each), so ptxas caps the kernel at 168
+// registers: the 128 f32 running sums fit, with a few bytes of spill.
+constexpr int kEpiWarps = 8;
+constexpr int kThreadsTc = (2 + kEpiWarps) * 32;
+// k-blocks per TMEM drain.  The tensor core truncates its f32 accumulator at
+// every K=16 step; draining every KC*BK = 1024 of K into round-to-nearest f32
+// register sums bounds that error by 64 * 2^-23 = 7.6e-6 relative for any K
+// (a single 8192-deep accumulation measured 3.1e-5, bound 6.1e-5).  Measured
+// at C5 (8192^3 bf16): KC=8 1340 TF/s, 16 1436, 32 1452, unchunked 1465.
+constexpr int KC = 16;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int GROUP_M = 8;                          // tile rasterisation: 8 M-blocks share B in L2
 
@@ -106,6 +117,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 // UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), sm_100 version bits.
 //   K-major  : rows of 128 B (64 bf16 along K), 8-row atoms 1024 B apart (SBO); LBO unused.
 //   MN-major : 64 MN-elements (128 B) per k-row, 8 k-rows per 1024 B atom; SBO = k-group
@@ -134,6 +158,11 @@ struct Params {
   int m, n, k;
   float alpha;
   int a_mn, b_mn;   // operand major-ness (1 = MN-contiguous)
+  int nkb;          // k-blocks per product
+  int nprod;        // 1 (bf16 operands) or 6 (f32 operands split into 3 bf16 planes)
+  int kplane;       // K offset between stacked planes (elements, multiple of BK)
+  uint32_t pa, pb;  // plane of A / B used by product p: bits [3p, 3p+3)
+  int kc;           // virtual k-blocks per TMEM drain (KC unless overridden)
 };
 
 __device__ __forceinline__ void tile_coords(int t, int ntm, int ntn, int &mb, int &nb) {
@@ -160,7 +189,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntm = (p.m + BM - 1) / BM, ntn = (p.n + BN - 1) / BN;
   const int ntiles = ntm * ntn;
-  const int nkb = (p.k + BK - 1) / BK;
+  const int nv = p.nprod * p.nkb;   // virtual k-blocks per tile (products x k-blocks)
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
@@ -171,7 +200,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);   // one arrive per epilogue warp
+      mbar_init(&tempty[a], kEpiWarps);   // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -186,7 +215,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {
-    // ===== TMA producer =====
+    // ===== TMA producer: virtual k-block v = product * nkb + kb =====
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -194,30 +223,33 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         int mb, nb;
         tile_coords(t, ntm, ntn, mb, nb);
         const int m0 = mb * BM, n0 = nb * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
+        int prod = 0, kb = 0;
+        for (int v = 0; v < nv; ++v, ++kb) {
+          if (kb == p.nkb) { kb = 0; ++prod; }
+          const int ka = (int)((p.pa >> (3 * prod)) & 7u) * p.kplane + kb * BK;
+          const int kbb = (int)((p.pb >> (3 * prod)) & 7u) * p.kplane + kb * BK;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * STAGE_BYTES;
           uint8_t *sb = sa + A_BYTES;
           mbar_expect_tx(&full[stage], STAGE_BYTES);
-          const int k0 = kb * BK;
           if (p.a_mn) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * (64 * BK * 2), &map_a, &full[stage], m0 + 64 * j, k0);
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * (64 * BK * 2), &map_a, &full[stage], m0 + 64 * j, ka);
           } else {
-            tma_load_2d(sa, &map_a, &full[stage], k0, m0);
+            tma_load_2d(sa, &map_a, &full[stage], ka, m0);
           }
           if (p.b_mn) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * (64 * BK * 2), &map_b, &full[stage], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * (64 * BK * 2), &map_b, &full[stage], n0 + 64 * j, kbb);
           } else {
-            tma_load_2d(sb, &map_b, &full[stage], k0, n0);
+            tma_load_2d(sb, &map_b, &full[stage], kbb, n0);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
+    // ===== MMA issuer: one TMEM accumulator per chunk of KC virtual k-blocks =====
     const uint32_t idesc = make_idesc(p.a_mn != 0, p.b_mn != 0);
     // per UMMA_K step: K-major advances 32 B inside the swizzled row;
     // MN-major advances two 1024-B k-groups.
@@ -225,60 +257,71 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const uint32_t a_lbo = p.a_mn ? 64u * BK * 2 : 16u, b_lbo = p.b_mn ? 64u * BK * 2 : 16u;
     int stage = 0;
     uint32_t phase = 0;
-    int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int acc = it & 1;
-      const uint32_t use = (uint32_t)(it >> 1);
-      mbar_wait(&tempty[acc], (use & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&full[stage], phase);
+    uint32_t gc = 0;   // chunks issued by this CTA (selects the TMEM buffer)
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int v0 = 0; v0 < nv; v0 += p.kc, ++gc) {
+        const int acc = (int)(gc & 1u);
+        const uint32_t use = gc >> 1;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        const int vend = min(nv, v0 + p.kc);
+        for (int v = v0; v < vend; ++v) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-            const uint64_t ad = make_desc(sa + kk * a_step, a_lbo, 1024u);
-            const uint64_t bd = make_desc(sb + kk * b_step, b_lbo, 1024u);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+              const uint64_t ad = make_desc(sa + kk * a_step, a_lbo, 1024u);
+              const uint64_t bd = make_desc(sb + kk * b_step, b_lbo, 1024u);
+              umma_bf16(d_tmem, ad, bd, idesc, (v != v0 || kk != 0) ? 1u : 0u);
+            }
+            umma_commit(&empty[stage]);                    // frees the smem slot when these MMAs finish
+            if (v == vend - 1) umma_commit(&tfull[acc]);   // chunk accumulated: hand it to the epilogue
           }
-          umma_commit(&empty[stage]);                       // frees the smem slot when these MMAs finish
-          if (kb == nkb - 1) umma_commit(&tfull[acc]);      // accumulator ready for the epilogue
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else {
-    // ===== epilogue: TMEM -> registers -> alpha * acc -> column-major stores =====
+    // ===== epilogue: drain each chunk into f32 register sums, then alpha * sum -> column-major stores =====
     const int q = warp & 3;                    // TMEM lane quarter this warp may access
-    int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int h = (warp - 2) >> 2;             // column half (128 columns)
+    uint32_t gc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, ntm, ntn, mb, nb);
-      const int acc = it & 1;
-      const uint32_t use = (uint32_t)(it >> 1);
-      mbar_wait(&tfull[acc], use & 1);
-      tc_fence_after();
-      const int row = mb * BM + q * 32 + lane;
-      const bool row_ok = row < p.m;
-      float *cp = p.c + row;
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + ch * 32), v);
-        if (ch == BN / 32 - 1) {               // accumulator drained: hand it back to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
-        const int col0 = nb * BN + ch * 32;
-        if (row_ok) {
+      float sum[BN / 2];
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < p.n) cp[(int64_t)(col0 + j) * p.ldc] = p.alpha * __uint_as_float(v[j]);
+      for (int j = 0; j < BN / 2; ++j) sum[j] = 0.0f;
+      for (int v0 = 0; v0 < nv; v0 += p.kc, ++gc) {
+        const int acc = (int)(gc & 1u);
+        const uint32_t use = gc >> 1;
+        mbar_wait(&tfull[acc], use & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + h * (BN / 2));
+#pragma unroll
+        for (int c4 = 0; c4 < BN / 64; ++c4) {
+          uint32_t v[32];
+          tmem_ld32_nowait(taddr + c4 * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sum[c4 * 32 + j] = __fadd_rn(sum[c4 * 32 + j], __uint_as_float(v[j]));
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);   // buffer drained: the MMA warp may reuse it
+      }
+      const int row = mb * BM + q * 32 + lane;
+      if (row < p.m) {
+        float *cp = p.c + row;
+        const int col0 = nb * BN + h * (BN / 2);
+#pragma unroll
+        for (int j = 0; j < BN / 2; ++j)
+          if (col0 + j < p.n) cp[(int64_t)(col0 + j) * p.ldc] = p.alpha * sum[j];
       }
     }
   }
@@ -288,6 +331,27 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// f32 -> three bf16 planes with x = hi + mid + lo + O(2^-24 |x|): each
+// residual is exact in f32 (Sterbenz), each plane the round-to-nearest bf16
+// of the residual.  Plane p of element (i, j) goes to out[p*plane_off + i + j*ld_out].
+__global__ void k_split3(const float *__restrict__ in, int64_t rows, int64_t cols, int64_t ld_in,
+                         uint16_t *__restrict__ out, int64_t ld_out, int64_t plane_off) {
+  const int64_t n = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / rows, i = e - j * rows;
+    const float x = in[i + j * ld_in];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    const float r1 = __fsub_rn(x, __bfloat162float(hi));
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const float r2 = __fsub_rn(r1, __bfloat162float(mid));
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r2);
+    const int64_t o = i + j * ld_out;
+    out[o] = __bfloat16_as_ushort(hi);
+    out[o + plane_off] = __bfloat16_as_ushort(mid);
+    out[o + 2 * plane_off] = __bfloat16_as_ushort(lo);
   }
 }
 
@@ -330,16 +394,55 @@ static int encode_map(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_
 
 }  // namespace tc
 
-// Tensor-core path for bf16 operands with an f32 result.  Other operand
-// types (and shapes TMA cannot describe) report handled = false and run on
-// the exact kernel.
+// Tensor-core path: bf16 operands directly; f32 operands split into three
+// bf16 planes each (k_split3) and multiplied as the six significant plane
+// products hi*hi, hi*mid, mid*hi, hi*lo, mid*mid, lo*hi in one kernel launch
+// (dropped terms are O(2^-24) relative).  Shapes TMA cannot describe report
+// handled = false and run on the exact kernel.
 bool gemm_tensor_supported(const fm_gemm_args &g) {
-  if (g.in_etype != FM_BF16 || g.out_etype != FM_F32) return false;
+  if (g.out_etype != FM_F32) return false;
+  if (g.m > INT32_MAX / 4 || g.n > INT32_MAX / 4 || g.k > INT32_MAX / 8) return false;
+  if (g.in_etype == FM_F32) return true;                                   // re-laid out by the split
+  if (g.in_etype != FM_BF16) return false;
   if ((((uintptr_t)g.a) & 15) || (((uintptr_t)g.b) & 15)) return false;   // TMA: 16-byte aligned base
   if ((g.lda * 2) % 16 || (g.ldb * 2) % 16) return false;                  // TMA: 16-byte multiple strides
-  if (g.m > INT32_MAX || g.n > INT32_MAX || g.k > INT32_MAX) return false;
   return true;
 }
+
+namespace {
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// split one f32 operand into stacked bf16 planes; returns the tensor-map
+// geometry of the stacked operand (inner extent, outer extent, ld)
+struct Planes {
+  uint16_t *buf = nullptr;
+  uint64_t inner = 0, outer = 0, ld = 0;
+};
+int split_operand(const float *src, int64_t rows, int64_t cols, int64_t ld_in, bool k_is_cols, int64_t kplane,
+                  Planes *pl, cudaStream_t s) {
+  int64_t ld_out, plane_off, bytes;
+  if (k_is_cols) {   // MN-major operand: planes appended along the column (K) dimension
+    ld_out = round_up(rows, 8);
+    plane_off = kplane * ld_out;
+    bytes = 3 * plane_off * 2;
+    pl->inner = (uint64_t)rows; pl->outer = (uint64_t)(3 * kplane);
+  } else {           // K-major operand: planes stacked along the row (K) dimension
+    ld_out = 3 * kplane;
+    plane_off = kplane;
+    bytes = ld_out * cols * 2;
+    pl->inner = (uint64_t)(3 * kplane); pl->outer = (uint64_t)cols;
+  }
+  pl->ld = (uint64_t)ld_out;
+  FM_CHECK(cudaMallocAsync((void **)&pl->buf, (size_t)bytes, s));
+  const int64_t kdim = k_is_cols ? cols : rows;
+  if (kdim != kplane) FM_CHECK(cudaMemsetAsync(pl->buf, 0, (size_t)bytes, s));   // zero K padding
+  const int64_t n = rows * cols;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8));
+  tc::k_split3<<<(unsigned)grid, 256, 0, s>>>(src, rows, cols, ld_in, pl->buf, ld_out, plane_off);
+  FM_CHECK_LAUNCH("f32 -> bf16 plane split kernel");
+  return 0;
+}
+}  // namespace
 
 int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
   using namespace tc;
@@ -352,26 +455,62 @@ int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
   p.alpha = (float)g.alpha;   // the scalar node is f32 in the tree (expr.py:225), applied in the epilogue
   p.a_mn = g.trans_a ? 0 : 1;   // op(A) = A (m x k, M-contiguous) or A^T of a k x m buffer (K-contiguous)
   p.b_mn = g.trans_b ? 1 : 0;   // op(B) = B (k x n, K-contiguous) or B^T of an n x k buffer (N-contiguous)
+  p.nkb = (int)((g.k + BK - 1) / BK);
+  static int kc_env = [] {
+    const char *e = getenv("FMB200_GEMM_KC");
+    return (e && *e) ? std::max(1, atoi(e)) : KC;
+  }();
+  p.kc = kc_env;
   CUtensorMap ma, mb;
   int st;
-  if (p.a_mn) st = encode_map(&ma, g.a, (uint64_t)g.m, (uint64_t)g.k, (uint64_t)g.lda, 64, BK);
-  else st = encode_map(&ma, g.a, (uint64_t)g.k, (uint64_t)g.m, (uint64_t)g.lda, BK, BM);
-  if (st) return st;
-  if (p.b_mn) st = encode_map(&mb, g.b, (uint64_t)g.n, (uint64_t)g.k, (uint64_t)g.ldb, 64, BK);
-  else st = encode_map(&mb, g.b, (uint64_t)g.k, (uint64_t)g.n, (uint64_t)g.ldb, BK, BN);
-  if (st) return st;
-
-  static bool attr_set = false;
-  if (!attr_set) {
-    FM_CHECK(cudaFuncSetAttribute(k_gemm_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr_set = true;
+  Planes pa, pb;
+  if (g.in_etype == FM_F32) {
+    const int64_t kplane = round_up(g.k, BK);
+    p.nprod = 6;
+    p.kplane = (int)kplane;
+    // products, smallest first: (0,2) (1,1) (2,0) (0,1) (1,0) (0,0)
+    const uint32_t A[6] = {0, 1, 2, 0, 1, 0}, B[6] = {2, 1, 0, 1, 0, 0};
+    p.pa = p.pb = 0;
+    for (int i = 0; i < 6; ++i) { p.pa |= A[i] << (3 * i); p.pb |= B[i] << (3 * i); }
+    st = p.a_mn ? split_operand((const float *)g.a, g.m, g.k, g.lda, true, kplane, &pa, s)
+                : split_operand((const float *)g.a, g.k, g.m, g.lda, false, kplane, &pa, s);
+    if (st) return st;
+    st = p.b_mn ? split_operand((const float *)g.b, g.n, g.k, g.ldb, true, kplane, &pb, s)
+                : split_operand((const float *)g.b, g.k, g.n, g.ldb, false, kplane, &pb, s);
+    if (st) { cudaFreeAsync(pa.buf, s); return st; }
+    st = encode_map(&ma, pa.buf, pa.inner, pa.outer, pa.ld, p.a_mn ? 64 : BK, p.a_mn ? BK : BM);
+    if (!st) st = encode_map(&mb, pb.buf, pb.inner, pb.outer, pb.ld, p.b_mn ? 64 : BK, p.b_mn ? BK : BN);
+  } else {
+    p.nprod = 1;
+    p.kplane = 0;
+    p.pa = p.pb = 0;
+    if (p.a_mn) st = encode_map(&ma, g.a, (uint64_t)g.m, (uint64_t)g.k, (uint64_t)g.lda, 64, BK);
+    else st = encode_map(&ma, g.a, (uint64_t)g.k, (uint64_t)g.m, (uint64_t)g.lda, BK, BM);
+    if (!st) {
+      if (p.b_mn) st = encode_map(&mb, g.b, (uint64_t)g.n, (uint64_t)g.k, (uint64_t)g.ldb, 64, BK);
+      else st = encode_map(&mb, g.b, (uint64_t)g.k, (uint64_t)g.n, (uint64_t)g.ldb, BK, BN);
+    }
   }
-  const int ntiles = (int)(((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN));
-  const int grid = std::min(ntiles, sm_count());
-  k_gemm_bf16<<<grid, kThreadsTc, SMEM_BYTES, s>>>(ma, mb, p);
-  FM_CHECK_LAUNCH("tcgen05 gemm kernel");
-  *handled = true;
-  return 0;
+  if (!st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(k_gemm_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+      if (e != cudaSuccess) st = fail("cudaFuncSetAttribute(k_gemm_bf16)", e);
+      else attr_set = true;
+    }
+  }
+  if (!st) {
+    const int ntiles = (int)(((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN));
+    const int grid = std::min(ntiles, sm_count());
+    k_gemm_bf16<<<grid, kThreadsTc, SMEM_BYTES, s>>>(ma, mb, p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) st = fail("tcgen05 gemm kernel", e);
+    else count_launch();
+  }
+  if (pa.buf) cudaFreeAsync(pa.buf, s);   // stream-ordered: released after the GEMM reads it
+  if (pb.buf) cudaFreeAsync(pb.buf, s);
+  if (!st) *handled = true;
+  return st;
 }
 
 }  // namespace fm
