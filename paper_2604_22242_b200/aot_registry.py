@@ -58,7 +58,24 @@ def hot_expressions() -> list[tuple[str, ast.ExprNode]]:
             ast.scalar_pre_mul(0.5, X),
             ast.scalar_add(ast.tanh(ast.scalar_pre_mul(coeff, ast.plus(
                 X, ast.scalar_pre_mul(0.044715, ast.pow_int(X, 3))))), 1))))
+    # the paper's add-N sweep (reference bench.py:307-326, Fig. 5):
+    # left-deep chains of N distinct inputs, one fused launch each
+    for ety in (ElemType.f32, ElemType.f64):
+        for k in range(5, 33):
+            mats = [_m(i, ety) for i in range(k)]
+            e = ast.plus(mats[0], mats[1])
+            for m in mats[2:]:
+                e = ast.plus(e, m)
+            out.append((f"add{k}N_{ety.value}", e))
     return out
+
+
+def vector_width(nin: int, ety: ElemType) -> int:
+    """Elements per thread chunk: a 32-byte (f32) / 32-byte (f64) run per
+    input, halved for wide chains so every input's loads fit in registers."""
+    if ety is ElemType.f32:
+        return 8 if nin <= 4 else 4
+    return 4 if nin <= 4 else 2
 
 
 # -- signature -> C++ expression-template type --------------------------------------
@@ -99,7 +116,7 @@ def cpp_type(node: ast.ExprNode) -> tuple[str, int, ElemType]:
     return text, len(ordinals), ety
 
 
-TEMPLATE_SHARDS = 6
+TEMPLATE_SHARDS = 8
 
 
 def generate(path: Path) -> Path:
@@ -138,7 +155,7 @@ def generate(path: Path) -> Path:
         sig = ast.signature_of(node)
         typ, nin, ety = cpp_type(node)
         T = "float" if ety is ElemType.f32 else "double"
-        V = 8 if ety is ElemType.f32 else 4
+        V = vector_width(nin, ety)
         lines.append(f"// {label}: {sig}")
         lines.append(f"using E{i} = TEval<{typ}, {T}, {nin}, {V}>;")
         lines.append(f"#if {i} % FM_TEMPLATE_SHARDS == FM_TEMPLATE_SHARD")

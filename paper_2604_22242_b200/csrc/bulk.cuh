@@ -23,7 +23,7 @@ namespace bulk {
 
 constexpr int kConsumerWarps = 16;
 constexpr int kBulkThreads = (kConsumerWarps + 1) * 32;
-constexpr int kChunkBytes = 16384;        // per input per stage
+constexpr int kChunkBytesMax = 16384;     // per input per stage (<= 4 inputs)
 constexpr int kSmemBudget = 192 * 1024;
 
 FM_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -69,6 +69,7 @@ template <class E>
 struct Geometry {
   using T = typename E::Elem;
   static constexpr int kNin = E::kNin;
+  static constexpr int kChunkBytes = kNin <= 4 ? kChunkBytesMax : kChunkBytesMax / 2;
   static constexpr int kChunk = kChunkBytes / (int)sizeof(T);               // elements per chunk
   static constexpr int kStagesRaw = kSmemBudget / (kChunkBytes * (kNin > 0 ? kNin : 1));
   static constexpr int kStages = kStagesRaw > 8 ? 8 : (kStagesRaw < 2 ? 2 : kStagesRaw);
@@ -76,6 +77,7 @@ struct Geometry {
   static constexpr int kW = 16 / (int)sizeof(T);                            // elements per vector
   static constexpr int kVecPerThread = kChunk / kW / (kConsumerWarps * 32);
   static_assert(kChunk % (kW * kConsumerWarps * 32) == 0, "chunk splits evenly over consumers");
+  static constexpr bool kOk = kNin <= 8 && kSmem <= 200 * 1024;             // fits the ring
 };
 
 // shared-memory ring: [stage][input] chunks, then full[S] / empty[S] mbarriers
@@ -86,10 +88,10 @@ struct Ring {
   uint64_t *full, *empty;
   FM_DEV explicit Ring(unsigned char *smem) {
     base = smem;
-    full = (uint64_t *)(smem + G::kStages * G::kNin * kChunkBytes);
+    full = (uint64_t *)(smem + G::kStages * G::kNin * G::kChunkBytes);
     empty = full + G::kStages;
   }
-  FM_DEV const unsigned char *chunk(int s, int i) const { return base + (s * G::kNin + i) * kChunkBytes; }
+  FM_DEV const unsigned char *chunk(int s, int i) const { return base + (s * G::kNin + i) * G::kChunkBytes; }
   FM_DEV void init() {
     if (threadIdx.x == 0) {
       for (int s = 0; s < G::kStages; ++s) {
@@ -109,10 +111,10 @@ struct Ring {
     for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++k) {
       const int s = (int)(k % S);
       if (k >= S) mbar_wait(&empty[s], (uint32_t)(((k / S) & 1) ^ 1));
-      mbar_expect_tx(&full[s], G::kNin * kChunkBytes);
+      mbar_expect_tx(&full[s], G::kNin * G::kChunkBytes);
 #pragma unroll
       for (int i = 0; i < G::kNin; ++i)
-        bulk_g2s((void *)chunk(s, i), (const T *)P.slots[i].ptr + c * G::kChunk, kChunkBytes, &full[s], pol);
+        bulk_g2s((void *)chunk(s, i), (const T *)P.slots[i].ptr + c * G::kChunk, G::kChunkBytes, &full[s], pol);
     }
   }
   // consumer: evaluate the kVecPerThread x kW elements of this thread in chunk stage s

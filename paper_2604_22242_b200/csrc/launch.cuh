@@ -9,6 +9,7 @@
 #include "common.cuh"
 #include "bulk.cuh"
 #include "skeletons.cuh"
+#include "tiled.cuh"
 
 namespace fm {
 
@@ -80,15 +81,69 @@ int run_copy_bulk(const fm_program &P, void *out, int64_t n_elem, cudaStream_t s
   return 0;
 }
 
+// Tiled, shared-memory staged VM copy (tiled.cuh): the widest column tile
+// whose double-buffered slot tiles fit in shared memory.
+template <class E, int TC>
+int launch_tiled(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s) {
+  using G = tiled::Geo<E::kV, TC, E::kWide ? 8 : 4>;
+  constexpr int kMaxSmem = 200 * 1024;
+  static int occ_slots = -1, occ_blocks = 0;
+  const int smem = (int)tiled::smem_bytes<E, TC>(P.n_slots);
+  static bool attr = false;
+  if (!attr) {
+    FM_CHECK(cudaFuncSetAttribute(tiled::k_copy_tiled<E, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    attr = true;
+  }
+  if (occ_slots != P.n_slots) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tiled::k_copy_tiled<E, TC>, G::NT, smem) != cudaSuccess ||
+        n < 1)
+      n = 1;
+    occ_slots = P.n_slots;
+    occ_blocks = n;
+  }
+  const int64_t ntiles = cdiv(n_rows, G::TR) * cdiv(n_cols, TC);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sm_count() * occ_blocks));
+  tiled::k_copy_tiled<E, TC><<<(unsigned)grid, G::NT, smem, s>>>(P, out, n_rows, n_cols);
+  FM_CHECK_LAUNCH("fused copy kernel (tiled)");
+  return 0;
+}
+
+template <class E>
+int run_copy_tiled(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s) {
+  constexpr int64_t kMaxSmem = 200 * 1024;
+  if (tiled::smem_bytes<E, 32>(P.n_slots) <= kMaxSmem) return launch_tiled<E, 32>(P, out, n_rows, n_cols, s);
+  if (tiled::smem_bytes<E, 16>(P.n_slots) <= kMaxSmem) return launch_tiled<E, 16>(P, out, n_rows, n_cols, s);
+  return launch_tiled<E, 8>(P, out, n_rows, n_cols, s);
+}
+
+// FMB200_TILED=0 disables the staged VM copy (A/B measurements)
+inline bool tiled_enabled() {
+  static int v = [] {
+    const char *e = getenv("FMB200_TILED");
+    return (e && *e) ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 template <class E>
 int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s) {
   constexpr int V = E::kV;
   if (n_rows == 0 || n_cols == 0) return 0;
+  if constexpr (E::kIsVm) {
+    // register VM: stage views / transposes through shared memory (for flat
+    // many-leaf programs the VM's per-instruction cost dominates and staging
+    // measured slower: add8N 3.5 -> 1.6 TB/s; those get AOT templates instead)
+    if (tiled_enabled() && !P.flat && n_rows * n_cols >= 4096)
+      return run_copy_tiled<E>(P, out, n_rows, n_cols, s);
+  }
   if constexpr (E::kFast) {
-    const int64_t n = n_rows * n_cols;
-    if (bulk_wanted(n * (E::kNin + 1) * (int64_t)sizeof(typename E::Elem), E::kHeavy) && P.n_slots == E::kNin &&
-        host_fast_ok<E>(P, out) && n >= (int64_t)bulk::Geometry<E>::kChunk * sm_count())
-      return run_copy_bulk<E>(P, out, n, s);
+    if constexpr (bulk::Geometry<E>::kOk) {
+      const int64_t n = n_rows * n_cols;
+      if (bulk_wanted(n * (E::kNin + 1) * (int64_t)sizeof(typename E::Elem), E::kHeavy) && P.n_slots == E::kNin &&
+          host_fast_ok<E>(P, out) && n >= (int64_t)bulk::Geometry<E>::kChunk * sm_count())
+        return run_copy_bulk<E>(P, out, n, s);
+    }
   }
   const int64_t nrb = cdiv(n_rows, V);
   const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;
@@ -122,10 +177,12 @@ int run_accu(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, int
              cudaStream_t s) {
   constexpr int V = E::kV;
   if constexpr (E::kFast) {
-    const int64_t n = n_rows * n_cols;
-    if (bulk_wanted(n * E::kNin * (int64_t)sizeof(typename E::Elem), E::kHeavy) && P.n_slots == E::kNin &&
-        host_fast_ok<E>(P, nullptr) && n >= (int64_t)bulk::Geometry<E>::kChunk * sm_count())
-      return run_accu_bulk<E>(P, out, n, finalize, s);
+    if constexpr (bulk::Geometry<E>::kOk) {
+      const int64_t n = n_rows * n_cols;
+      if (bulk_wanted(n * E::kNin * (int64_t)sizeof(typename E::Elem), E::kHeavy) && P.n_slots == E::kNin &&
+          host_fast_ok<E>(P, nullptr) && n >= (int64_t)bulk::Geometry<E>::kChunk * sm_count())
+        return run_accu_bulk<E>(P, out, n, finalize, s);
+    }
   }
   const int64_t nrb = cdiv(n_rows, V);
   const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;

@@ -96,7 +96,10 @@ struct TEval {
   using Elem = T;
   static constexpr int kV = V;
   static constexpr int kNin = NIN;
-  static constexpr bool kFast = true;
+  // warp-tile fast path (a second tile of every input in flight) up to 8
+  // inputs; wider chains (add-N) load all inputs of a chunk at once instead
+  static constexpr bool kFast = NIN <= 8;
+  static constexpr bool kIsVm = false;
   static constexpr bool kHeavy = Heavy<Expr>::v;
 
   FM_DEV static T ev_elem(const fm_program &P, const T (&x)[NIN]) {

@@ -60,6 +60,11 @@ struct Chunk {
   int64_t col;
   int cnt;        // valid elements (<= V)
   bool flat;
+  // shared-memory staged tile (tiled.cuh), or nullptr: read global memory
+  const unsigned char *stage = nullptr;
+  int tr = 0, tc = 0;        // chunk position inside the tile (first row, column)
+  int trp = 0, tcp = 0;      // element pitches of the column-major / transposed layouts
+  int slot_bytes = 0;        // bytes per staged slot
 };
 
 // Load V elements of slot s for the chunk.
@@ -119,12 +124,67 @@ FM_DEV void load_slot(const fm_slot &s, const Chunk &ch, uint32_t (&lo)[V], uint
   }
 }
 
+// Load V elements of slot `s` from its staged tile.  Untransposed slots are
+// staged column-major (element (r, c) at c*trp + r), transposed ones
+// row-major (at r*tcp + c), so both are read along the layout they were
+// copied in with (coalesced global reads, tiled.cuh).
+template <int V>
+FM_DEV void load_staged(const fm_slot &s, const unsigned char *buf, const Chunk &ch, uint32_t (&lo)[V],
+                        uint32_t (&hi)[V]) {
+  const int w = s.etype == FM_F64 ? 8 : (s.etype == FM_BF16 ? 2 : 4);
+  if (!s.transposed) {
+    const unsigned char *p = buf + (size_t)(ch.tc * ch.trp + ch.tr) * w;
+    if (w == 4 && V % 4 == 0) {
+#pragma unroll
+      for (int q = 0; q < V / 4; ++q) {
+        const uint4 x = *(const uint4 *)(p + 16 * q);
+        lo[4 * q] = x.x; lo[4 * q + 1] = x.y; lo[4 * q + 2] = x.z; lo[4 * q + 3] = x.w;
+      }
+      return;
+    }
+    if (w == 8 && V % 2 == 0) {
+#pragma unroll
+      for (int q = 0; q < V / 2; ++q) {
+        const uint4 x = *(const uint4 *)(p + 16 * q);
+        lo[2 * q] = x.x; hi[2 * q] = x.y; lo[2 * q + 1] = x.z; hi[2 * q + 1] = x.w;
+      }
+      return;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) lo[v] = ((uint32_t)((const uint16_t *)p)[v]) << 16;
+    return;
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const unsigned char *p = buf + (size_t)((ch.tr + v) * ch.tcp + ch.tc) * w;
+    if (w == 8) {
+      const uint2 x = *(const uint2 *)p;
+      lo[v] = x.x; hi[v] = x.y;
+    } else if (w == 4) {
+      lo[v] = *(const uint32_t *)p;
+    } else {
+      lo[v] = ((uint32_t)*(const uint16_t *)p) << 16;
+    }
+  }
+}
+
+// Slot j of the program for the chunk: staged tile when the kernel staged it
+// (every slot but diagonals), global memory otherwise.
+template <int V>
+FM_DEV void fetch_slot(const fm_program &P, int j, const Chunk &ch, uint32_t (&lo)[V], uint32_t (&hi)[V]) {
+  const fm_slot &s = P.slots[j];
+  if (ch.stage && s.map != FM_MAP_DIAG) load_staged<V>(s, ch.stage + (size_t)j * ch.slot_bytes, ch, lo, hi);
+  else load_slot<V>(s, ch, lo, hi);
+}
+
 // -----------------------------------------------------------------------------
 // The interpreter.  WIDE: registers carry 64-bit values (any f64 in the
 // program).  MAXD: stack depth.  V: elements per thread.  NPF: prefetched slots.
 template <bool WIDE, int MAXD, int V, int NPF>
 struct Vm {
   static constexpr int kV = V;
+  static constexpr bool kWide = WIDE;
+  static constexpr bool kIsVm = true;
   static constexpr bool kFast = false;
   FM_DEV static bool fast_ok(const fm_program &, const void *) { return false; }
   static constexpr int HD = WIDE ? MAXD : 1;
@@ -142,7 +202,7 @@ struct Vm {
     for (int j = 0; j < NPF; ++j) {
       if (j < P.n_slots) {
         uint32_t th[V];
-        load_slot<V>(P.slots[j], ch, plo[j], th);
+        fetch_slot<V>(P, j, ch, plo[j], th);
         if constexpr (WIDE) {
 #pragma unroll
           for (int v = 0; v < V; ++v) phi[j < HP ? j : 0][v] = th[v];
@@ -164,7 +224,7 @@ struct Vm {
       case 1: if constexpr (NPF > 1) { VLOOP LO(D)[v] = plo[1 % NPF][v]; break; } \
       case 2: if constexpr (NPF > 2) { VLOOP LO(D)[v] = plo[2 % NPF][v]; break; } \
       case 3: if constexpr (NPF > 3) { VLOOP LO(D)[v] = plo[3 % NPF][v]; break; } \
-      default: { uint32_t th[V]; load_slot<V>(P.slots[a], ch, LO(D), th); }    \
+      default: { uint32_t th[V]; fetch_slot<V>(P, a, ch, LO(D), th); }         \
     }                                                                           \
   } break;
 
@@ -178,7 +238,7 @@ struct Vm {
         default: VLOOP { LO(D)[v] = plo[3 % NPF][v]; HI(D)[v] = phi[3 % HP][v]; } break; \
       }                                                                         \
     } else {                                                                    \
-      load_slot<V>(P.slots[a], ch, LO(D), HI(D));                               \
+      fetch_slot<V>(P, a, ch, LO(D), HI(D));                                    \
     }                                                                           \
   } break;
 
