@@ -58,6 +58,22 @@ def hot_expressions() -> list[tuple[str, ast.ExprNode]]:
             ast.scalar_pre_mul(0.5, X),
             ast.scalar_add(ast.tanh(ast.scalar_pre_mul(coeff, ast.plus(
                 X, ast.scalar_pre_mul(0.044715, ast.pow_int(X, 3))))), 1))))
+    # paper suite members with views / transposes (bench.py:119-147): leaves
+    # read through index maps; copies run on the tiled staged skeleton
+    _B = MatShape(8, 8)
+    for ety in (ElemType.f32, ElemType.f64):
+        t = ety.value
+        X, Y, Z, W = (ast.leaf(i, ety, _B) for i in range(4))
+        ch = [ast.subview(i, ety, 2, 2, MatShape(4, 4), _B) for i in range(4)]
+        out.append((f"addsub2_{t}", ast.plus(ch[0], ch[1])))
+        out.append((f"addsub4_{t}", ast.plus(ast.plus(ast.plus(ch[0], ch[1]), ch[2]), ch[3])))
+        out.append((f"expr1_{t}", ast.plus(ast.scalar_pre_mul(2, ast.plus(ast.transpose(X), Y)),
+                                          ast.scalar_pre_mul(2, ast.plus(X, ast.transpose(Y))))))
+        out.append((f"expr2_{t}", ast.plus(ast.plus(ast.scalar_pre_mul(2.0, X),
+                                                    ast.transpose(ast.plus(Y, Z))),
+                                           ast.log(ast.pow_int(W, 2)))))
+        d = [ast.diag(i, ety, k, _B) for i, k in ((0, -1), (0, 1), (1, -1), (1, 1))]
+        out.append((f"diagsum_{t}", ast.schur(ast.plus(d[0], d[1]), ast.plus(d[2], d[3]))))
     # the paper's add-N sweep (reference bench.py:307-326, Fig. 5):
     # left-deep chains of N distinct inputs, one fused launch each
     for ety in (ElemType.f32, ElemType.f64):
@@ -89,31 +105,51 @@ _SC = {ast.UnaryKind.scalar_add: "SAdd", ast.UnaryKind.scalar_pre_mul: "SMul",
 
 
 def cpp_type(node: ast.ExprNode) -> tuple[str, int, ElemType]:
-    """C++ type, number of distinct inputs and the common element type."""
-    ordinals: dict[int, int] = {}
+    """C++ type, number of leaf slots and the common element type.
+
+    `In<j>` reads program slot j.  Slots are numbered exactly as
+    lower.py numbers them: first visit in pre-order of the key (input
+    ordinal, index map, transposed, view occurrence), with a Transpose node
+    flipping the orientation of the leaves below it (it has no node of its
+    own: the transposition lives in the slot's index map)."""
+    inputs: dict[int, int] = {}
+    views: dict[int, int] = {}
+    slots: dict[tuple, int] = {}
     slot = [0]
     ety = node.etype
 
-    def go(n) -> str:
+    def leaf_slot(n, tr: bool) -> int:
+        i = inputs.setdefault(n.mat_id, len(inputs))
+        v = -1
+        if not isinstance(n, ast.Leaf):
+            v = views.get(i, 0)
+            views[i] = v + 1
+        kind = 0 if isinstance(n, ast.Leaf) else (1 if isinstance(n, ast.Subview) else 2)
+        return slots.setdefault((i, kind, tr, v), len(slots))
+
+    def go(n, tr=False) -> str:
         if n.etype is not ety:
             raise ValueError("templates need a single element type")
-        if isinstance(n, ast.Leaf):
-            return f"In<{ordinals.setdefault(n.mat_id, len(ordinals))}>"
+        if isinstance(n, (ast.Leaf, ast.Subview, ast.Diag)):
+            return f"In<{leaf_slot(n, tr)}>"
+        if isinstance(n, ast.Transpose):
+            return go(n.child, not tr)
         if isinstance(n, ast.BinaryElem):
-            return f"{_BIN[n.kind]}<{go(n.left)}, {go(n.right)}>"
+            left = go(n.left, tr)
+            return f"{_BIN[n.kind]}<{left}, {go(n.right, tr)}>"
         if isinstance(n, ast.UnaryElem):
             if n.kind in _SC:
                 s = slot[0]
                 slot[0] += 1
-                return f"{_SC[n.kind]}<{s}, {go(n.child)}>"
+                return f"{_SC[n.kind]}<{s}, {go(n.child, tr)}>"
             if n.kind is ast.UnaryKind.pow_int:
-                return f"Pow<{n.exponent}, {go(n.child)}>"
+                return f"Pow<{n.exponent}, {go(n.child, tr)}>"
             if n.kind in _UN:
-                return f"{_UN[n.kind]}<{go(n.child)}>"
+                return f"{_UN[n.kind]}<{go(n.child, tr)}>"
         raise ValueError(f"no template for {type(n).__name__}")
 
     text = go(node)
-    return text, len(ordinals), ety
+    return text, len(slots), ety
 
 
 TEMPLATE_SHARDS = 8
@@ -151,18 +187,23 @@ def generate(path: Path) -> Path:
         "",
     ]
     entries = []
-    for i, (label, node) in enumerate(hot_expressions()):
+    types: dict[str, int] = {}      # one instantiation per distinct evaluator type
+    for label, node in hot_expressions():
         sig = ast.signature_of(node)
         typ, nin, ety = cpp_type(node)
         T = "float" if ety is ElemType.f32 else "double"
         V = vector_width(nin, ety)
+        full = f"TEval<{typ}, {T}, {nin}, {V}>"
         lines.append(f"// {label}: {sig}")
-        lines.append(f"using E{i} = TEval<{typ}, {T}, {nin}, {V}>;")
-        lines.append(f"#if {i} % FM_TEMPLATE_SHARDS == FM_TEMPLATE_SHARD")
-        lines.append(f"FM_INST(E{i}, )")
-        lines.append("#else")
-        lines.append(f"FM_INST(E{i}, extern)")
-        lines.append("#endif")
+        if full not in types:
+            i = types[full] = len(types)
+            lines.append(f"using E{i} = {full};")
+            lines.append(f"#if {i} % FM_TEMPLATE_SHARDS == FM_TEMPLATE_SHARD")
+            lines.append(f"FM_INST(E{i}, )")
+            lines.append("#else")
+            lines.append(f"FM_INST(E{i}, extern)")
+            lines.append("#endif")
+        i = types[full]
         entries.append(f'  {{"{sig}", &t_copy<E{i}>, &t_accu<E{i}>, &t_dim<E{i}>, {nin}, {ety.code}}},')
     lines.append("")
     lines.append("#if FM_TEMPLATE_SHARD == 0")

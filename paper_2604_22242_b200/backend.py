@@ -362,7 +362,7 @@ class B200Backend(Backend):
         prog = lw.lower(node)
         schema = tuple(source.schema) if source.schema is not None else arg_schema(node, skeleton)
         kid = ctypes.c_int(-1)
-        if self.use_templates and prog.flat:
+        if self.use_templates:
             self.nat.call("fm_kernel_lookup", source.signature.encode(), ctypes.byref(kid))
         tmpl = FmProgram()
         tmpl.n_instr = len(prog.code)

@@ -122,7 +122,7 @@ int fm_launch_copy(int kernel_id, const fm_program *prog, void *out, int64_t n_r
   cudaStream_t s = (cudaStream_t)stream;
   if (kernel_id >= 0) {
     const TemplateEntry *e = entry_for(kernel_id, SK_COPY);
-    if (!e || !prog->flat) return fail_msg("copy: kernel id does not match a flat template");
+    if (!e || e->n_inputs != prog->n_slots) return fail_msg("copy: kernel id does not match the program");
     return e->copy(*prog, out, n_rows, n_cols, s);
   }
   return vm_dispatch<CopyF>(*prog, out, n_rows, n_cols, s);
@@ -135,7 +135,7 @@ int fm_launch_accu(int kernel_id, const fm_program *prog, void *out, int64_t n_r
   cudaStream_t s = (cudaStream_t)stream;
   if (kernel_id >= 0) {
     const TemplateEntry *e = entry_for(kernel_id, SK_ACCU);
-    if (!e || !prog->flat) return fail_msg("accu: kernel id does not match a flat template");
+    if (!e || e->n_inputs != prog->n_slots) return fail_msg("accu: kernel id does not match the program");
     return e->accu(*prog, out, n_rows, n_cols, finalize, s);
   }
   return vm_dispatch<AccuF>(*prog, out, n_rows, n_cols, (int)finalize, s);
@@ -156,7 +156,7 @@ int fm_launch_reduce_dim(int kernel_id, const fm_program *prog, int32_t dim, int
   cudaStream_t s = (cudaStream_t)stream;
   if (kernel_id >= 0) {
     const TemplateEntry *e = entry_for(kernel_id, dim == 0 ? SK_DIM0 : SK_DIM1);
-    if (!e || !prog->flat) return fail_msg("reduce_dim: kernel id does not match a flat template");
+    if (!e || e->n_inputs != prog->n_slots) return fail_msg("reduce_dim: kernel id does not match the program");
     return e->reduce_dim(*prog, dim, n_rows, n_cols, R, s);
   }
   return vm_dispatch<DimF>(*prog, (int)dim, n_rows, n_cols, R, s);

@@ -130,13 +130,11 @@ template <class E>
 int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s) {
   constexpr int V = E::kV;
   if (n_rows == 0 || n_cols == 0) return 0;
-  if constexpr (E::kIsVm) {
-    // register VM: stage views / transposes through shared memory (for flat
-    // many-leaf programs the VM's per-instruction cost dominates and staging
-    // measured slower: add8N 3.5 -> 1.6 TB/s; those get AOT templates instead)
-    if (tiled_enabled() && !P.flat && n_rows * n_cols >= 4096)
-      return run_copy_tiled<E>(P, out, n_rows, n_cols, s);
-  }
+  // views / transposes (VM or template): stage through shared memory (for
+  // flat many-leaf programs on the VM, staging measured slower -- add8N 3.5
+  // -> 1.6 TB/s, the VM's per-instruction cost dominates -- so the add-N
+  // chains get AOT templates instead)
+  if (tiled_enabled() && !P.flat && n_rows * n_cols >= 4096) return run_copy_tiled<E>(P, out, n_rows, n_cols, s);
   if constexpr (E::kFast) {
     if constexpr (bulk::Geometry<E>::kOk) {
       const int64_t n = n_rows * n_cols;

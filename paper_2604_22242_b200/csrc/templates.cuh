@@ -100,6 +100,7 @@ struct TEval {
   // inputs; wider chains (add-N) load all inputs of a chunk at once instead
   static constexpr bool kFast = NIN <= 8;
   static constexpr bool kIsVm = false;
+  static constexpr bool kWide = sizeof(T) == 8;
   static constexpr bool kHeavy = Heavy<Expr>::v;
 
   FM_DEV static T ev_elem(const fm_program &P, const T (&x)[NIN]) {
@@ -111,7 +112,7 @@ struct TEval {
   FM_DEV static void eval(const fm_program &P, const Chunk &ch, uint32_t (&lo)[V], uint32_t (&hi)[V]) {
     uint32_t xl[NIN][V], xh[NIN][V];
 #pragma unroll
-    for (int i = 0; i < NIN; ++i) load_slot<V>(P.slots[i], ch, xl[i], xh[i]);
+    for (int i = 0; i < NIN; ++i) fetch_slot<V>(P, i, ch, xl[i], xh[i]);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       T xv[NIN];

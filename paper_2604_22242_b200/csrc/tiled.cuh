@@ -49,46 +49,67 @@ struct Geo {
   static constexpr int TR = 8 * V;               // 8 row-chunks of V elements per column
   static constexpr int NT = 8 * TC;              // one thread per (row-chunk, column)
   static constexpr int TRP = TR + 8;             // column-major pitch: 16-byte column starts for w = 2, 4, 8
-  static constexpr int TCP = TC + 1;             // row-major pitch: odd, so column reads spread over banks
+  static constexpr int TCP = TC;                 // row-major pitch (16-byte chunks swizzled, see stage_tile)
+  static constexpr int LTR = V == 8 ? 6 : (V == 4 ? 5 : 4);   // log2(TR)
+  static constexpr int LTC = TC == 32 ? 5 : (TC == 16 ? 4 : 3);
   static constexpr int SB0 = (TC * TRP > TR * TCP ? TC * TRP : TR * TCP) * WMAX;
   static constexpr int SLOT_BYTES = (SB0 + 15) / 16 * 16;
 };
 
 // Issue the copies of tile (r0, c0) for every staged slot into `buf`.
+// Full tiles with 16-byte aligned source runs move 16-byte vectors (index
+// math by shifts: TR, TC and the widths are powers of two); edge tiles and
+// unaligned views copy element by element.
 template <int V, int TC, int WMAX>
 FM_DEV void stage_tile(const fm_program &P, unsigned char *buf, int64_t r0, int64_t c0, int rv, int cv) {
   using G = Geo<V, TC, WMAX>;
   const int tid = threadIdx.x;
+  const bool full = rv == G::TR && cv == TC;
   for (int j = 0; j < P.n_slots; ++j) {
     const fm_slot &s = P.slots[j];
     if (s.map == FM_MAP_DIAG) continue;
     const int w = etype_width(s.etype);
+    const int lw = w == 8 ? 3 : (w == 4 ? 2 : 1);
     unsigned char *dst = buf + (size_t)j * G::SLOT_BYTES;
     const unsigned char *base = (const unsigned char *)s.ptr;
+    const bool aligned = ((s.ld * w) & 15) == 0 && (((uintptr_t)base) & 15) == 0;
     if (!s.transposed) {
       // element (r, c) of the tile = parent (r0 + r + row_off, c0 + c + col_off); columns contiguous
       const int64_t prow = r0 + s.row_off, pcol = c0 + s.col_off;
-      const bool vec = ((rv * w) & 15) == 0 && ((prow * w) & 15) == 0 && ((s.ld * w) & 15) == 0 &&
-                       (((uintptr_t)base) & 15) == 0;
-      if (vec) {
-        const int per_col = rv * w / 16;
-        for (int i = tid; i < per_col * cv; i += G::NT) {
-          const int c = i / per_col, q = i - c * per_col;
-          cp_async16(dst + (size_t)c * G::TRP * w + 16 * q, base + ((prow + (int64_t)(pcol + c) * s.ld) * w) + 16 * q);
+      const unsigned char *src0 = base + (prow + pcol * s.ld) * w;
+      if (full && aligned && ((prow * w) & 15) == 0) {
+        const int lpc = (G::LTR + lw) - 4;                 // log2(16-byte vectors per column)
+        for (int i = tid; i < (TC << lpc); i += G::NT) {
+          const int c = i >> lpc, q = i & ((1 << lpc) - 1);
+          cp_async16(dst + ((size_t)c * G::TRP << lw) + 16 * q, src0 + (int64_t)c * s.ld * w + 16 * q);
         }
       } else {
         for (int i = tid; i < rv * cv; i += G::NT) {
           const int c = i / rv, r = i - c * rv;
-          copy_elem(dst + (size_t)(c * G::TRP + r) * w, base + (prow + r + (int64_t)(pcol + c) * s.ld) * w, w);
+          copy_elem(dst + (size_t)(c * G::TRP + r) * w, src0 + (r + (int64_t)c * s.ld) * w, w);
         }
       }
     } else {
-      // transposed: element (r, c) = parent (c0 + c + row_off, r0 + r + col_off); parent columns
-      // run along the tile's rows, so copy tile rows (contiguous in the parent) into a row-major tile
+      // transposed: element (r, c) = parent (c0 + c + row_off, r0 + r + col_off); parent columns run
+      // along the tile's rows, so tile row r is a contiguous run of the parent.  Row-major tile,
+      // pitch TC, 16-byte chunks XOR-swizzled by (r / 8) so a warp's column reads spread over banks.
       const int64_t prow = c0 + s.row_off, pcol = r0 + s.col_off;
-      for (int i = tid; i < rv * cv; i += G::NT) {
-        const int r = i / cv, c = i - r * cv;
-        copy_elem(dst + (size_t)(r * G::TCP + c) * w, base + (prow + c + (int64_t)(pcol + r) * s.ld) * w, w);
+      const unsigned char *src0 = base + (prow + pcol * s.ld) * w;
+      if (full && aligned && ((prow * w) & 15) == 0) {
+        const int lpr = (G::LTC + lw) - 4;                 // log2(16-byte vectors per row)
+        const int qmask = (1 << lpr) - 1;
+        for (int i = tid; i < (G::TR << lpr); i += G::NT) {
+          const int r = i >> lpr, q = i & qmask;
+          const int qs = q ^ ((r >> 3) & qmask);
+          cp_async16(dst + ((size_t)r * TC << lw) + 16 * qs, src0 + (int64_t)r * s.ld * w + 16 * q);
+        }
+      } else {
+        for (int i = tid; i < rv * cv; i += G::NT) {
+          const int r = i / cv, c = i - r * cv;
+          const int qmask = (TC * w / 16) - 1;
+          const int byte = c * w, qs = (byte >> 4) ^ ((r >> 3) & qmask);
+          copy_elem(dst + (size_t)r * TC * w + qs * 16 + (byte & 15), src0 + (c + (int64_t)r * s.ld) * w, w);
+        }
       }
     }
   }

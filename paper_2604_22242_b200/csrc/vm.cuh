@@ -154,9 +154,13 @@ FM_DEV void load_staged(const fm_slot &s, const unsigned char *buf, const Chunk 
     for (int v = 0; v < V; ++v) lo[v] = ((uint32_t)((const uint16_t *)p)[v]) << 16;
     return;
   }
+  // row-major tile, pitch tcp elements, 16-byte chunks XOR-swizzled by row/8
+  const int qmask = (ch.tcp * w / 16) - 1;
+  const int byte = ch.tc * w;
 #pragma unroll
   for (int v = 0; v < V; ++v) {
-    const unsigned char *p = buf + (size_t)((ch.tr + v) * ch.tcp + ch.tc) * w;
+    const int r = ch.tr + v;
+    const unsigned char *p = buf + (size_t)r * ch.tcp * w + ((((byte >> 4) ^ (r >> 3)) & qmask) << 4) + (byte & 15);
     if (w == 8) {
       const uint2 x = *(const uint2 *)p;
       lo[v] = x.x; hi[v] = x.y;
