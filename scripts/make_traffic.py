@@ -24,6 +24,8 @@ LABELS = {
     "c3_copy_f32": "ncu_c3_copy",
     "c4_colstats_f64": "ncu_c4_colstats",
     "c5_gemm_bf16": "ncu_c5_gemm",
+    "c5_gemm_f32": "ncu_c5f32_gemm",
+    "expr1": "ncu_suite_expr1",
 }
 
 
