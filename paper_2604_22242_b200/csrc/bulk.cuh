@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<E> ring(smem_raw);
   ring.init();
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5;
   const int64_t nfull = n_elem / C;
   if (warp == kConsumerWarps) {
@@ -216,6 +218,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   __shared__ bool last;
   Ring<E> ring(smem_raw);
   ring.init();
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nfull = n_elem / C;
   double acc = 0.0;

@@ -76,7 +76,8 @@ int run_copy_bulk(const fm_program &P, void *out, int64_t n_elem, cudaStream_t s
   }
   const int64_t chunks = n_elem / G::kChunk;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, sm_count()));
-  bulk::k_copy_bulk<E><<<(unsigned)grid, bulk::kBulkThreads, G::kSmem, s>>>(P, out, n_elem);
+  FM_CHECK(launch_pdl(bulk::k_copy_bulk<E>, dim3((unsigned)grid), dim3(bulk::kBulkThreads), G::kSmem, s, P, out,
+                      n_elem));
   FM_CHECK_LAUNCH("fused copy kernel (bulk)");
   return 0;
 }
@@ -146,7 +147,7 @@ int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cud
   const int64_t nrb = cdiv(n_rows, V);
   const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;
   const int64_t grid = wave_grid<GridTag<E, 0>>(k_copy<E>, cdiv(nch, kThreads));
-  k_copy<E><<<(unsigned)grid, kThreads, 0, s>>>(P, out, n_rows, n_cols);
+  FM_CHECK(launch_pdl(k_copy<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, P, out, n_rows, n_cols));
   FM_CHECK_LAUNCH("fused copy kernel");
   return 0;
 }
@@ -164,8 +165,8 @@ int run_accu_bulk(const fm_program &P, void *out, int64_t n_elem, int finalize, 
   Scratch sc;
   int st = get_scratch((void *)s, grid * sizeof(double) + 64, &sc);
   if (st) return st;
-  bulk::k_accu_bulk<E><<<(unsigned)grid, bulk::kBulkThreads, G::kSmem, s>>>(P, out, n_elem, finalize,
-                                                                            (double *)sc.payload, sc.counters);
+  FM_CHECK(launch_pdl(bulk::k_accu_bulk<E>, dim3((unsigned)grid), dim3(bulk::kBulkThreads), G::kSmem, s, P, out,
+                      n_elem, finalize, (double *)sc.payload, sc.counters));
   FM_CHECK_LAUNCH("fused accu kernel (bulk)");
   return 0;
 }
@@ -190,7 +191,8 @@ int run_accu(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, int
   if (st) return st;
   double *pd = (double *)sc.payload;
   uint32_t *pu = (uint32_t *)(pd + grid);
-  k_accu<E><<<(unsigned)grid, kThreads, 0, s>>>(P, out, n_rows, n_cols, finalize, pd, pu, sc.counters);
+  FM_CHECK(launch_pdl(k_accu<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, P, out, n_rows, n_cols, finalize, pd,
+                      pu, sc.counters));
   FM_CHECK_LAUNCH("fused accu kernel");
   return 0;
 }
@@ -205,7 +207,7 @@ int run_reduce_dim(const fm_program &P, int dim, int64_t n_rows, int64_t n_cols,
   if (dim == 0) {
     // one persistent wave; columns are the work units (C4: 16384 / 444)
     const int64_t grid = wave_grid<GridTag<E, 2>>(k_reduce_cols<E>, n_cols);
-    k_reduce_cols<E><<<(unsigned)grid, kThreads, 0, s>>>(P, R, n_rows, n_cols);
+    FM_CHECK(launch_pdl(k_reduce_cols<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, P, R, n_rows, n_cols));
     FM_CHECK_LAUNCH("fused column-reduction kernel");
     return 0;
   }

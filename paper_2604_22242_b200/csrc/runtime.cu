@@ -1,6 +1,7 @@
 // runtime.cu -- device, memory, stream, event entry points of the C ABI and
 // the shared scratch / error plumbing (include/fmb200.h).
 #include <atomic>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -24,6 +25,14 @@ int fail_msg(const std::string &msg) {
   return -1;
 }
 void count_launch(int64_t n) { g_launches += n; }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("FMB200_PDL");
+    return !(e && *e && atoi(e) == 0);
+  }();
+  return on;
+}
 
 int sm_count() {
   static int cached[64] = {0};

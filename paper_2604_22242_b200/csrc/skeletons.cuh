@@ -113,6 +113,8 @@ template <class E>
 __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ fm_program P, void *out,
                                                    int64_t n_rows, int64_t n_cols) {
   constexpr int V = E::kV;
+  pdl_trigger();
+  pdl_wait();
   const int64_t n_elem = n_rows * n_cols;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -241,6 +243,8 @@ __global__ void __launch_bounds__(kThreads) k_accu(const __grid_constant__ fm_pr
   __shared__ bool last;
   const int rt = P.result_etype;
   const bool fl = is_float_etype(rt);
+  pdl_trigger();
+  pdl_wait();
   int64_t nrb;
   const int64_t nch = chunk_count<V>(P, n_rows, n_cols, nrb);
   const int64_t n_elem = n_rows * n_cols;
@@ -435,6 +439,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_reduce_cols(const __grid_consta
   const int rt = P.result_etype;
   const bool fl = is_float_etype(rt);
   const unsigned need = needed_stats(R);
+  pdl_trigger();
+  pdl_wait();
   bool fast = false;
   int64_t fast_rows = 0;
   if constexpr (E::kFast) {
