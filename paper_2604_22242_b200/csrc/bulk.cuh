@@ -13,8 +13,15 @@
 // coalesced st.global.  Bytes in flight per SM = (stages-1) x chunk x inputs,
 // independent of the consumers' register use.
 //
-// Persistent: one CTA per SM, chunks assigned round-robin.  The ragged tail
-// (< one chunk) is evaluated by the consumers with the general chunk path.
+// Persistent: one CTA per SM.  SMs drain HBM at visibly different rates
+// (ncu, profiles/r01/ncu_c2_accu_f32: per-SM active cycles 175K..229K for
+// equal static shares), so only a static head of the chunks is assigned
+// round-robin; the rest are claimed dynamically (one atomicAdd per chunk,
+// fetched a chunk ahead by the producer), so fast SMs take more.  Copies are
+// deterministic regardless; reductions keep a fixed summation order by
+// summing the static head per CTA and each dynamic chunk into its own
+// partial slot, combined in chunk order.  The ragged tail (< one chunk) is
+// evaluated by the consumers with the general chunk path.
 #pragma once
 #include "skeletons.cuh"
 
@@ -73,7 +80,7 @@ struct Geometry {
   static constexpr int kChunk = kChunkBytes / (int)sizeof(T);               // elements per chunk
   static constexpr int kStagesRaw = kSmemBudget / (kChunkBytes * (kNin > 0 ? kNin : 1));
   static constexpr int kStages = kStagesRaw > 8 ? 8 : (kStagesRaw < 2 ? 2 : kStagesRaw);
-  static constexpr int kSmem = kStages * kNin * kChunkBytes + 2 * kStages * 8 + 128;
+  static constexpr int kSmem = kStages * kNin * kChunkBytes + 3 * kStages * 8 + 128;
   static constexpr int kW = 16 / (int)sizeof(T);                            // elements per vector
   static constexpr int kVecPerThread = kChunk / kW / (kConsumerWarps * 32);
   static_assert(kChunk % (kW * kConsumerWarps * 32) == 0, "chunk splits evenly over consumers");
@@ -86,10 +93,12 @@ struct Ring {
   using G = Geometry<E>;
   unsigned char *base;
   uint64_t *full, *empty;
+  int64_t *cid;          // chunk held by each stage (-1: no more chunks)
   FM_DEV explicit Ring(unsigned char *smem) {
     base = smem;
     full = (uint64_t *)(smem + G::kStages * G::kNin * G::kChunkBytes);
     empty = full + G::kStages;
+    cid = (int64_t *)(empty + G::kStages);
   }
   FM_DEV const unsigned char *chunk(int s, int i) const { return base + (s * G::kNin + i) * G::kChunkBytes; }
   FM_DEV void init() {
@@ -102,20 +111,38 @@ struct Ring {
     }
     __syncthreads();
   }
-  // producer: one elected lane streams chunks c = blockIdx.x + k*gridDim.x
-  FM_DEV void produce(const fm_program &P, int64_t nfull) {
+  // producer (one elected lane): the static head, chunks blockIdx.x + j*grid
+  // for j < nstat, then dynamic chunks nstat*grid + atomicAdd(ctr, 1) until
+  // nfull, then a sentinel stage (cid = -1, plain arrive).
+  FM_DEV void produce(const fm_program &P, int64_t nfull, int64_t nstat, unsigned *ctr) {
     using T = typename E::Elem;
     constexpr int S = G::kStages;
     const uint64_t pol = evict_first_policy();
     int64_t k = 0;
-    for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++k) {
-      const int s = (int)(k % S);
-      if (k >= S) mbar_wait(&empty[s], (uint32_t)(((k / S) & 1) ^ 1));
+    auto stage_for = [&](int64_t kk) {
+      const int s = (int)(kk % S);
+      if (kk >= S) mbar_wait(&empty[s], (uint32_t)(((kk / S) & 1) ^ 1));
+      return s;
+    };
+    auto issue = [&](int64_t c) {
+      const int s = stage_for(k++);
+      cid[s] = c;
       mbar_expect_tx(&full[s], G::kNin * G::kChunkBytes);
 #pragma unroll
       for (int i = 0; i < G::kNin; ++i)
         bulk_g2s((void *)chunk(s, i), (const T *)P.slots[i].ptr + c * G::kChunk, G::kChunkBytes, &full[s], pol);
+    };
+    for (int64_t j = 0; j < nstat; ++j) issue(blockIdx.x + j * gridDim.x);
+    const int64_t dbase = nstat * gridDim.x;
+    int64_t c = dbase + atomicAdd(ctr, 1u);
+    while (c < nfull) {
+      const int64_t next = dbase + atomicAdd(ctr, 1u);   // claim ahead: the atomic overlaps the slot wait
+      issue(c);
+      c = next;
     }
+    const int s = stage_for(k);
+    cid[s] = -1;
+    mbar_arrive(&full[s]);
   }
   // consumer: evaluate the kVecPerThread x kW elements of this thread in chunk stage s
   FM_DEV void eval(const fm_program &P, int s, int ctid, typename E::Elem (&r)[G::kVecPerThread][G::kW]) const {
@@ -147,7 +174,7 @@ struct Ring {
 
 template <class E>
 __global__ void __launch_bounds__(kBulkThreads, 1)
-    k_copy_bulk(const __grid_constant__ fm_program P, void *out, int64_t n_elem) {
+    k_copy_bulk(const __grid_constant__ fm_program P, void *out, int64_t n_elem, unsigned *counters) {
   using G = Geometry<E>;
   using T = typename E::Elem;
   constexpr int S = G::kStages, C = G::kChunk;
@@ -158,15 +185,16 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   pdl_wait();
   const int warp = threadIdx.x >> 5;
   const int64_t nfull = n_elem / C;
+  unsigned *ctr = counters, *done = counters + 1;
   if (warp == kConsumerWarps) {
-    if ((threadIdx.x & 31) == 0) ring.produce(P, nfull);
-    return;
-  }
+    if ((threadIdx.x & 31) == 0) ring.produce(P, nfull, 0, ctr);   // all dynamic: copies are order-free
+  } else {
   const int ctid = threadIdx.x;   // 0 .. kConsumerWarps*32-1
-  int64_t k = 0;
-  for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++k) {
+  for (int64_t k = 0;; ++k) {
     const int s = (int)(k % S);
     mbar_wait(&ring.full[s], (uint32_t)((k / S) & 1));
+    const int64_t c = ring.cid[s];
+    if (c < 0) break;
     T r[G::kVecPerThread][G::kW];
     ring.eval(P, s, ctid, r);
     ring.release(s);   // smem reads done: free the stage before the long-latency stores
@@ -199,22 +227,37 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
       store_chunk<V>(out, P.result_etype, ch.base, ch.cnt, lo, hi);
     }
   }
+  }
+  // the last CTA out resets the chunk counter for the next launch on this stream
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      *ctr = 0u;
+      *done = 0u;
+    }
+  }
 }
 
 
 // Fused full reduction over bulk-staged chunks: per-thread f64 accumulation
-// (the reduce_accu accumulator type, codegen.py:47-49), block tree, per-block
-// partial, last-block finish -- one launch, deterministic for a grid.
+// (the reduce_accu accumulator type, codegen.py:47-49).  The static head is
+// summed per CTA (warp trees + block tree -> part_d[cta]); every dynamic chunk
+// gets its own partial (warp trees, then one thread over the warps in order
+// -> part_c[chunk - head]).  The last CTA combines part_d in CTA order and
+// part_c in chunk order: one launch, and the result does not depend on which
+// CTA claimed which dynamic chunk.
 template <class E>
 __global__ void __launch_bounds__(kBulkThreads, 1)
     k_accu_bulk(const __grid_constant__ fm_program P, void *out, int64_t n_elem, int finalize,
-                double *part_d, unsigned *counter) {
+                double *part_d, double *part_c, int64_t nstat, unsigned *counters) {
   using G = Geometry<E>;
   using T = typename E::Elem;
   constexpr int S = G::kStages, C = G::kChunk;
   constexpr int NW = kConsumerWarps;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double smd[NW];
+  __shared__ double wsum[2][NW];
   __shared__ bool last;
   Ring<E> ring(smem_raw);
   ring.init();
@@ -222,22 +265,44 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nfull = n_elem / C;
+  const int64_t dbase = nstat * gridDim.x;
+  unsigned *done = counters, *ctr = counters + 1;
   double acc = 0.0;
   if (warp == NW) {
-    if (lane == 0) ring.produce(P, nfull);
+    if (lane == 0) ring.produce(P, nfull, nstat, ctr);
   } else {
     const int ctid = threadIdx.x;
-    int64_t k = 0;
-    for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x, ++k) {
+    int par = 0;
+    for (int64_t k = 0;; ++k) {
       const int s = (int)(k % S);
       mbar_wait(&ring.full[s], (uint32_t)((k / S) & 1));
+      const int64_t c = ring.cid[s];
+      if (c < 0) break;
       T r[G::kVecPerThread][G::kW];
       ring.eval(P, s, ctid, r);
       ring.release(s);
+      if (c < dbase) {
 #pragma unroll
-      for (int j = 0; j < G::kVecPerThread; ++j)
+        for (int j = 0; j < G::kVecPerThread; ++j)
 #pragma unroll
-        for (int e = 0; e < G::kW; ++e) acc = add_d(acc, (double)r[j][e]);
+          for (int e = 0; e < G::kW; ++e) acc = add_d(acc, (double)r[j][e]);
+      } else {
+        double a = 0.0;
+#pragma unroll
+        for (int j = 0; j < G::kVecPerThread; ++j)
+#pragma unroll
+          for (int e = 0; e < G::kW; ++e) a = add_d(a, (double)r[j][e]);
+        a = warp_sum_d(a);
+        if (lane == 0) wsum[par][warp] = a;
+        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");   // consumer warps only
+        if (ctid == 0) {
+          double t = 0.0;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) t = add_d(t, wsum[par][w]);
+          part_c[c - dbase] = t;
+        }
+        par ^= 1;
+      }
     }
     if (blockIdx.x == gridDim.x - 1) {   // ragged tail (< one chunk): general path
       constexpr int V = E::kV;
@@ -264,20 +329,31 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     for (int w = 0; w < NW; ++w) b = add_d(b, smd[w]);
     part_d[blockIdx.x] = b;
     __threadfence();
-    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    last = (atomicAdd(done, 1u) == gridDim.x - 1);
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (warp == 0) {
-    double sd = 0.0;
-    for (int i = lane; i < (int)gridDim.x; i += 32) sd = add_d(sd, ((volatile double *)part_d)[i]);
-    sd = warp_sum_d(sd);
-    if (lane == 0) {
-      if (finalize == FM_FINAL_SQRT) sd = sqrt_d(sd);
-      *(double *)out = sd;
-      *counter = 0u;
-    }
+  // combine: per-CTA partials then per-chunk partials, each thread over a
+  // fixed strided subset, then fixed trees
+  const int64_t ndyn = nfull - dbase;
+  double sd = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += kBulkThreads) sd = add_d(sd, ((volatile double *)part_d)[i]);
+  double sc = 0.0;
+  for (int64_t i = threadIdx.x; i < ndyn; i += kBulkThreads) sc = add_d(sc, ((volatile double *)part_c)[i]);
+  sd = warp_sum_d(sd);
+  sc = warp_sum_d(sc);
+  __shared__ double fin_d[kBulkThreads / 32], fin_c[kBulkThreads / 32];
+  if (lane == 0) { fin_d[warp] = sd; fin_c[warp] = sc; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < kBulkThreads / 32; ++w) { a = add_d(a, fin_d[w]); b = add_d(b, fin_c[w]); }
+    double total = add_d(a, b);
+    if (finalize == FM_FINAL_SQRT) total = sqrt_d(total);
+    *(double *)out = total;
+    *done = 0u;
+    *ctr = 0u;
   }
 }
 

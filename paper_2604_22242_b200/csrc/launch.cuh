@@ -76,8 +76,11 @@ int run_copy_bulk(const fm_program &P, void *out, int64_t n_elem, cudaStream_t s
   }
   const int64_t chunks = n_elem / G::kChunk;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, sm_count()));
+  Scratch sc;
+  int st = get_scratch((void *)s, 64, &sc);
+  if (st) return st;
   FM_CHECK(launch_pdl(bulk::k_copy_bulk<E>, dim3((unsigned)grid), dim3(bulk::kBulkThreads), G::kSmem, s, P, out,
-                      n_elem));
+                      n_elem, sc.counters));
   FM_CHECK_LAUNCH("fused copy kernel (bulk)");
   return 0;
 }
@@ -162,11 +165,16 @@ int run_accu_bulk(const fm_program &P, void *out, int64_t n_elem, int finalize, 
   }
   const int64_t chunks = n_elem / G::kChunk;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, sm_count()));
+  // static head: 80 % of the chunks round-robin (summed per CTA), the rest
+  // claimed dynamically with one partial slot each
+  const int64_t nstat = chunks * 4 / 5 / grid;
+  const int64_t ndyn = chunks - nstat * grid;
   Scratch sc;
-  int st = get_scratch((void *)s, grid * sizeof(double) + 64, &sc);
+  int st = get_scratch((void *)s, (grid + ndyn) * sizeof(double) + 64, &sc);
   if (st) return st;
+  double *part_d = (double *)sc.payload;
   FM_CHECK(launch_pdl(bulk::k_accu_bulk<E>, dim3((unsigned)grid), dim3(bulk::kBulkThreads), G::kSmem, s, P, out,
-                      n_elem, finalize, (double *)sc.payload, sc.counters));
+                      n_elem, finalize, part_d, part_d + grid, nstat, sc.counters));
   FM_CHECK_LAUNCH("fused accu kernel (bulk)");
   return 0;
 }

@@ -109,6 +109,20 @@ FM_DEV int64_t chunk_count(const fm_program &P, int64_t n_rows, int64_t n_cols, 
 // issued before the current tile's math) when the program is flat and
 // 16-byte aligned; the ragged remainder (and every other program) uses the
 // general chunk path.
+// prefetch depth of the copy fast path (FM_COPY_DEPTH2_HEAVY=0 at build
+// time keeps every chain at depth 1)
+#ifndef FM_COPY_DEPTH2_HEAVY
+#define FM_COPY_DEPTH2_HEAVY 1
+#endif
+template <class E>
+constexpr int kCopyDepth() {
+  // measured (bench.py --config c3 / suite): C3 (2 inputs, exp) 6.24 -> 6.44
+  // TB/s at depth 2; single-input heavy chains (sigmoid, swish, gelu) lose
+  // 2-4 % to the extra registers
+  if constexpr (E::kFast) return (FM_COPY_DEPTH2_HEAVY && E::kHeavy && E::kNin >= 2) ? 2 : 1;
+  else return 1;
+}
+
 template <class E>
 __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ fm_program P, void *out,
                                                    int64_t n_rows, int64_t n_cols) {
@@ -125,12 +139,25 @@ __global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ fm_pr
       const int64_t nwarp = stride >> 5;
       const int64_t ntile = n_elem / kTile;
       int64_t t = c >> 5;
-      typename E::Buf buf;
-      if (t < ntile) E::load_tile(P, t * kTile, lane, buf);
-      for (; t < ntile; t += nwarp) {
-        const typename E::Buf cur = buf;
-        if (t + nwarp < ntile) E::load_tile(P, (t + nwarp) * kTile, lane, buf);
-        E::copy_tile(P, out, t * kTile, lane, cur);
+      if constexpr (kCopyDepth<E>() == 2) {
+        // long per-element math: two tiles in flight per warp
+        typename E::Buf b0, b1;
+        if (t < ntile) E::load_tile(P, t * kTile, lane, b0);
+        if (t + nwarp < ntile) E::load_tile(P, (t + nwarp) * kTile, lane, b1);
+        for (; t < ntile; t += nwarp) {
+          const typename E::Buf cur = b0;
+          b0 = b1;
+          if (t + 2 * nwarp < ntile) E::load_tile(P, (t + 2 * nwarp) * kTile, lane, b1);
+          E::copy_tile(P, out, t * kTile, lane, cur);
+        }
+      } else {
+        typename E::Buf buf;
+        if (t < ntile) E::load_tile(P, t * kTile, lane, buf);
+        for (; t < ntile; t += nwarp) {
+          const typename E::Buf cur = buf;
+          if (t + nwarp < ntile) E::load_tile(P, (t + nwarp) * kTile, lane, buf);
+          E::copy_tile(P, out, t * kTile, lane, cur);
+        }
       }
       c += ntile * 32;   // ragged remainder: flat V-element chunks from here on
     }

@@ -131,3 +131,17 @@ def test_empty_and_degenerate(ctx):
     assert fm.accu(one * one) == 12.25
     v = fm.randu(1, 100_003, 1, "f64", ctx)          # a row vector: ragged, flat
     assert fm.accu(v) == pytest.approx(orc.accu(orc.randu(1, 100_003, 1, "f64"), fm.ElemType.f64), rel=1e-13)
+
+
+@pytest.mark.parametrize("etype", ["f32", "f64"])
+def test_bulk_staged_copy_beyond_l2(ctx, etype):
+    """A light chain whose working set (>= 512 MiB) takes the TMA-bulk-staged
+    copy with dynamically claimed chunks, with a ragged tail (< one chunk)."""
+    n_rows, n_cols = 8191, 8193 if etype == "f32" else 6001
+    X, Y = fm.randu(n_rows, n_cols, 5, etype, ctx), fm.randu(n_rows, n_cols, 6, etype, ctx)
+    Z = fm.Mat(n_rows, n_cols, etype, ctx)
+    for _ in range(2):                       # the chunk counter resets between launches
+        Z.assign(2 * (X % Y) + X)
+    x, y = X.to_numpy(), Y.to_numpy()
+    t = x.dtype.type(2)
+    assert np.array_equal(Z.to_numpy(), t * (x * y) + x)
