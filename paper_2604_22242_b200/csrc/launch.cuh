@@ -38,13 +38,12 @@ int64_t wave_grid(K kernel, int64_t work_blocks) {
 template <class E, int Skel> struct GridTag {};
 
 // Streaming path choice for an eligible template (flat, 16-byte aligned):
-// TMA-bulk staging (bulk.cuh) once the working set is well beyond L2 --
-// measured on B200 (profiles/r01): a light 2R+1W chain at 32768^2 runs
-// 5.47 TB/s on register tiles vs 6.49 TB/s bulk-staged, while at 4096^2
-// (1.5x L2) register tiles win (7.06 vs 6.89 TB/s).  Chains with a
-// transcendental are issue-bound rather than latency-bound and stay on
-// register tiles (C3: 6.22 vs 6.18 TB/s).  FMB200_BULK=0 / 1 forces one path
-// for every eligible template (A/B measurements).
+// TMA-bulk staging with dynamically claimed chunks (bulk.cuh) once the
+// working set is well beyond L2.  Measured on B200 (profiles/r01): light
+// 2R+1W chain at 32768^2 7.03 TB/s bulk vs 5.47 on register tiles; C3 7.02
+// vs 6.44; C2 reductions 7.15 step; at 4096^2 (1.5x L2) register tiles win
+// (7.06 vs 6.89).  Chains flagged RegTiles (tanh, elementwise division) stay
+// on register tiles.  FMB200_BULK=0 / 1 forces one path (A/B measurements).
 inline int bulk_override() {
   static int v = [] {
     const char *e = getenv("FMB200_BULK");
@@ -53,9 +52,9 @@ inline int bulk_override() {
   return v;
 }
 constexpr int64_t kBulkMinBytes = 512ll << 20;
-inline bool bulk_wanted(int64_t working_set_bytes, bool heavy) {
+inline bool bulk_wanted(int64_t working_set_bytes, bool reg_tiles) {
   const int ov = bulk_override();
-  return ov >= 0 ? ov == 1 : (!heavy && working_set_bytes >= kBulkMinBytes);
+  return ov >= 0 ? ov == 1 : (!reg_tiles && working_set_bytes >= kBulkMinBytes);
 }
 
 template <class E>
@@ -142,7 +141,7 @@ int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cud
   if constexpr (E::kFast) {
     if constexpr (bulk::Geometry<E>::kOk) {
       const int64_t n = n_rows * n_cols;
-      if (bulk_wanted(n * (E::kNin + 1) * (int64_t)sizeof(typename E::Elem), E::kHeavy) && P.n_slots == E::kNin &&
+      if (bulk_wanted(n * (E::kNin + 1) * (int64_t)sizeof(typename E::Elem), E::kRegTiles) && P.n_slots == E::kNin &&
           host_fast_ok<E>(P, out) && n >= (int64_t)bulk::Geometry<E>::kChunk * sm_count())
         return run_copy_bulk<E>(P, out, n, s);
     }
@@ -186,7 +185,7 @@ int run_accu(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, int
   if constexpr (E::kFast) {
     if constexpr (bulk::Geometry<E>::kOk) {
       const int64_t n = n_rows * n_cols;
-      if (bulk_wanted(n * E::kNin * (int64_t)sizeof(typename E::Elem), E::kHeavy) && P.n_slots == E::kNin &&
+      if (bulk_wanted(n * E::kNin * (int64_t)sizeof(typename E::Elem), E::kRegTiles) && P.n_slots == E::kNin &&
           host_fast_ok<E>(P, nullptr) && n >= (int64_t)bulk::Geometry<E>::kChunk * sm_count())
         return run_accu_bulk<E>(P, out, n, finalize, s);
     }

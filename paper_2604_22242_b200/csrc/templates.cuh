@@ -86,6 +86,29 @@ template <class A, class B> struct Heavy<Sub<A, B>> { static constexpr bool v = 
 template <class A, class B> struct Heavy<Mul<A, B>> { static constexpr bool v = Heavy<A>::v || Heavy<B>::v; };
 template <class A, class B> struct Heavy<Div<A, B>> { static constexpr bool v = Heavy<A>::v || Heavy<B>::v; };
 
+// RegTiles<Expr>::v -- stream on register tiles even beyond L2: the chains
+// whose per-element math is longest (tanh, an elementwise division) need the
+// register path's 32-40 resident warps to hide it; the bulk skeleton runs 16
+// consumer warps per SM.  Measured at 10000^2 f32 (bench.py --config suite):
+// swish 4.02 (tiles) vs 3.44 TB/s (bulk), gelu 2.03 vs 1.84, while sigmoid
+// (scalar division) 3.99 vs 4.52 and C3 6.44 vs 7.02 favour bulk.
+template <class X> struct RegTiles { static constexpr bool v = false; };
+template <class A> struct RegTiles<Tanh<A>> { static constexpr bool v = true; };
+template <class A, class B> struct RegTiles<Div<A, B>> { static constexpr bool v = true; };
+template <class A> struct RegTiles<Exp<A>> { static constexpr bool v = RegTiles<A>::v; };
+template <class A> struct RegTiles<Log<A>> { static constexpr bool v = RegTiles<A>::v; };
+template <class A> struct RegTiles<Neg<A>> { static constexpr bool v = RegTiles<A>::v; };
+template <class A> struct RegTiles<Abs<A>> { static constexpr bool v = RegTiles<A>::v; };
+template <class A> struct RegTiles<Sqrt<A>> { static constexpr bool v = RegTiles<A>::v; };
+template <int K, class A> struct RegTiles<Pow<K, A>> { static constexpr bool v = RegTiles<A>::v; };
+template <int S, class A> struct RegTiles<SAdd<S, A>> { static constexpr bool v = RegTiles<A>::v; };
+template <int S, class A> struct RegTiles<SMul<S, A>> { static constexpr bool v = RegTiles<A>::v; };
+template <int S, class A> struct RegTiles<SDiv<S, A>> { static constexpr bool v = RegTiles<A>::v; };
+template <int S, class A> struct RegTiles<Gts<S, A>> { static constexpr bool v = RegTiles<A>::v; };
+template <class A, class B> struct RegTiles<Add<A, B>> { static constexpr bool v = RegTiles<A>::v || RegTiles<B>::v; };
+template <class A, class B> struct RegTiles<Sub<A, B>> { static constexpr bool v = RegTiles<A>::v || RegTiles<B>::v; };
+template <class A, class B> struct RegTiles<Mul<A, B>> { static constexpr bool v = RegTiles<A>::v || RegTiles<B>::v; };
+
 // Evaluator over a chunk: all NIN inputs share type T (f32 or f64), and so
 // does the result.  eval() is the general path (any index map, ragged
 // chunks); the *_tile members serve the steady state of a flat program whose
@@ -102,6 +125,7 @@ struct TEval {
   static constexpr bool kIsVm = false;
   static constexpr bool kWide = sizeof(T) == 8;
   static constexpr bool kHeavy = Heavy<Expr>::v;
+  static constexpr bool kRegTiles = RegTiles<Expr>::v;
 
   FM_DEV static T ev_elem(const fm_program &P, const T (&x)[NIN]) {
     return Expr::template ev<T>(x, P.scalars);
