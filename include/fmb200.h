@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FMB200_ABI_VERSION 1
+#define FMB200_ABI_VERSION 2
 
 /* element types (exprtree.ElemType.code) */
 enum {
@@ -122,7 +122,14 @@ typedef struct {
 /* accu finalisers */
 enum { FM_FINAL_NONE = 0, FM_FINAL_SQRT = 1 };
 
-/* GEMM arguments: C[m x n] = alpha * op(A) @ op(B), all column-major. */
+/* GEMM arguments, all column-major:
+ *   T   = round_out(alpha * op(A) @ op(B))
+ *   C   = T                                              (c_in == NULL)
+ *   C   = round_out(round_out(alpha2 * T) + round_out(beta * C_in))   (epilogue)
+ * The epilogue is the elementwise step the reference plans as a separate
+ * fused launch after its MatMulStep (e.g. `2*(A@B) + C`, plan.py:171-205),
+ * with the same per-operation rounding; C_in may alias C (read then written
+ * by the same thread). */
 typedef struct {
   const void *a;  int64_t lda;  int32_t trans_a;
   const void *b;  int64_t ldb;  int32_t trans_b;
@@ -133,6 +140,10 @@ typedef struct {
   int32_t out_etype;   /* FM_F32 (bf16/f32 inputs) or FM_F64 */
   int32_t precision;   /* FM_GEMM_* */
   int32_t reserved;
+  const void *c_in;    /* epilogue addend (out_etype), or NULL */
+  int64_t ld_c_in;
+  double alpha2;       /* epilogue scale of the rounded product (1 = none) */
+  double beta;         /* epilogue scale of c_in */
 } fm_gemm_args;
 
 enum {

@@ -69,6 +69,8 @@ class FmGemmArgs(ctypes.Structure):
         ("alpha", ctypes.c_double),
         ("in_etype", ctypes.c_int32), ("out_etype", ctypes.c_int32),
         ("precision", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("c_in", ctypes.c_void_p), ("ld_c_in", ctypes.c_int64),
+        ("alpha2", ctypes.c_double), ("beta", ctypes.c_double),
     ]
 
 

@@ -473,7 +473,8 @@ class B200Backend(Backend):
 
     def _gemm_args(self, out: BufferHandle, a: BufferHandle, b: BufferHandle, m: int, n: int, k: int,
                    trans_a: bool, trans_b: bool, alpha: float, lda: int | None, ldb: int | None,
-                   precision: int) -> FmGemmArgs:
+                   precision: int, c_in: BufferHandle | None = None, alpha2: float = 1.0,
+                   beta: float = 0.0) -> FmGemmArgs:
         if a.etype is not b.etype or not a.etype.is_float:
             raise BackendError("gemm operands must share a float element type")
         args = FmGemmArgs()
@@ -490,12 +491,22 @@ class B200Backend(Backend):
         need_a, need_b = args.lda * (m if trans_a else k), args.ldb * (k if trans_b else n)
         if a.n_elem < need_a or b.n_elem < need_b or out.n_elem < m * n:
             raise BackendError("gemm buffer smaller than its operand")
+        args.alpha2, args.beta = alpha2, beta
+        if c_in is not None:
+            if c_in.etype is not out.etype or c_in.n_elem < m * n:
+                raise BackendError("gemm epilogue addend must match the output type and shape")
+            args.c_in, args.ld_c_in = self.ptr(c_in), m
         return args
 
     def gemm(self, out: BufferHandle, a: BufferHandle, b: BufferHandle, m: int, n: int, k: int,
              trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0,
-             lda: int | None = None, ldb: int | None = None, precision: int = 0) -> None:
-        args = self._gemm_args(out, a, b, m, n, k, trans_a, trans_b, alpha, lda, ldb, precision)
+             lda: int | None = None, ldb: int | None = None, precision: int = 0,
+             c_in: BufferHandle | None = None, alpha2: float = 1.0, beta: float = 0.0) -> None:
+        """out = alpha * op(a) @ op(b), or with an addend
+        out = alpha2 * (alpha * op(a) @ op(b)) + beta * c_in (each product and
+        the sum rounded to the output type)."""
+        args = self._gemm_args(out, a, b, m, n, k, trans_a, trans_b, alpha, lda, ldb, precision,
+                               c_in, alpha2, beta)
         self.nat.call("fm_gemm", ctypes.byref(args), self.stream)
         self.launch_count += 1
 

@@ -71,8 +71,15 @@ __global__ void __launch_bounds__(256) k_gemm_exact(fm_gemm_args g) {
       if (i < g.m && j < g.n) {
         double v = acc[a][b];
         if (g.alpha != 1.0) v = __dmul_rn(g.alpha, v);
-        if (g.out_etype == FM_F64) ((double *)g.c)[i + j * g.ldc] = v;
-        else ((float *)g.c)[i + j * g.ldc] = __double2float_rn(v);
+        if (g.out_etype == FM_F64) {
+          if (g.c_in) v = __dadd_rn(__dmul_rn(g.alpha2, v), __dmul_rn(g.beta, ((const double *)g.c_in)[i + j * g.ld_c_in]));
+          ((double *)g.c)[i + j * g.ldc] = v;
+        } else {
+          float t = __double2float_rn(v);
+          if (g.c_in)
+            t = __fadd_rn(__fmul_rn((float)g.alpha2, t), __fmul_rn((float)g.beta, ((const float *)g.c_in)[i + j * g.ld_c_in]));
+          ((float *)g.c)[i + j * g.ldc] = t;
+        }
       }
     }
 }
@@ -120,8 +127,9 @@ extern "C" int fm_gemm(const fm_gemm_args *args, void *stream) {
   if ((g.in_etype == FM_F64) != (g.out_etype == FM_F64)) return fail_msg("gemm: f64 in <-> f64 out");
   if (g.out_etype != FM_F32 && g.out_etype != FM_F64) return fail_msg("gemm: output must be f32 or f64");
   if (g.m == 0 || g.n == 0) return 0;
+  if (g.c_in && g.ld_c_in < g.m) return fail_msg("gemm: ld_c_in < m");
   cudaStream_t s = (cudaStream_t)stream;
-  if (g.k == 0) {
+  if (g.k == 0 && !g.c_in) {
     const size_t w = g.out_etype == FM_F64 ? 8 : 4;
     for (int64_t j = 0; j < g.n; ++j) FM_CHECK(cudaMemsetAsync((char *)g.c + j * g.ldc * w, 0, g.m * w, s));
     return 0;

@@ -163,6 +163,9 @@ struct Params {
   int kplane;       // K offset between stacked planes (elements, multiple of BK)
   uint32_t pa, pb;  // plane of A / B used by product p: bits [3p, 3p+3)
   int kc;           // virtual k-blocks per TMEM drain (KC unless overridden)
+  const float *cin; // epilogue addend (nullptr: none)
+  int64_t ldcin;
+  float alpha2, beta;
 };
 
 __device__ __forceinline__ void tile_coords(int t, int ntm, int ntn, int &mb, int &nb) {
@@ -319,9 +322,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       if (row < p.m) {
         float *cp = p.c + row;
         const int col0 = nb * BN + h * (BN / 2);
+        if (p.cin) {
+          const float *ci = p.cin + row;
 #pragma unroll
-        for (int j = 0; j < BN / 2; ++j)
-          if (col0 + j < p.n) cp[(int64_t)(col0 + j) * p.ldc] = p.alpha * sum[j];
+          for (int j = 0; j < BN / 2; ++j)
+            if (col0 + j < p.n) {
+              const float t = __fmul_rn(p.alpha, sum[j]);
+              cp[(int64_t)(col0 + j) * p.ldc] =
+                  __fadd_rn(__fmul_rn(p.alpha2, t), __fmul_rn(p.beta, ci[(int64_t)(col0 + j) * p.ldcin]));
+            }
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN / 2; ++j)
+            if (col0 + j < p.n) cp[(int64_t)(col0 + j) * p.ldc] = p.alpha * sum[j];
+        }
       }
     }
   }
@@ -453,6 +467,10 @@ int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
   p.ldc = g.ldc;
   p.m = (int)g.m; p.n = (int)g.n; p.k = (int)g.k;
   p.alpha = (float)g.alpha;   // the scalar node is f32 in the tree (expr.py:225), applied in the epilogue
+  p.cin = (const float *)g.c_in;
+  p.ldcin = g.ld_c_in;
+  p.alpha2 = (float)g.alpha2;
+  p.beta = (float)g.beta;
   p.a_mn = g.trans_a ? 0 : 1;   // op(A) = A (m x k, M-contiguous) or A^T of a k x m buffer (K-contiguous)
   p.b_mn = g.trans_b ? 1 : 0;   // op(B) = B (k x n, K-contiguous) or B^T of an n x k buffer (N-contiguous)
   p.nkb = (int)((g.k + BK - 1) / BK);

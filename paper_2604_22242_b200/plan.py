@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 
 from .errors import PlanError
 from .exprtree import (
-    AliasKind, BinaryElem, Diag, ElemType, ExprNode, InputSpec, Leaf, MatMul,
+    AliasKind, BinaryElem, BinaryKind, Diag, ElemType, ExprNode, InputSpec, Leaf, MatMul,
     MatShape, Reduce, ReduceKind, ScalarSlot, Subview, Transpose, UnaryElem,
     UnaryKind, aliases, collect_inputs, signature_of,
 )
@@ -113,6 +113,11 @@ class GemmStep:
     in_etype: ElemType
     out_etype: ElemType
     out_shape: MatShape
+    # epilogue: out = alpha2 * (alpha * A@B) + beta * C, each op rounded to
+    # out_etype -- the elementwise step after the product, folded in
+    c_id: int | None = None
+    alpha2: float = 1.0
+    beta: float = 0.0
 
     @property
     def m(self) -> int:
@@ -244,10 +249,66 @@ class _Planner:
         raise PlanError(f"cannot plan node {type(node).__name__}")
 
 
+def _scaled(node: ExprNode) -> tuple[ExprNode, float]:
+    """Peel scalar pre-multiplies: node = s * rest."""
+    s = 1.0
+    while isinstance(node, UnaryElem) and node.kind is UnaryKind.scalar_pre_mul:
+        s *= float(node.scalar)
+        node = node.child
+    return node, s
+
+
+def _product_epilogue(node: ExprNode):
+    """`s2 * (A @ B) (+|-) sb * C` -> (MatMul, alpha2, C leaf, beta), or None.
+
+    Folds the elementwise step the reference runs as a separate fused launch
+    after its MatMulStep into the GEMM epilogue.  Only an f32/f64 product with
+    a dense same-shape addend of the output type folds; the epilogue rounds
+    alpha2*T, beta*C and their sum to the output type, as the reference's
+    copy kernel would (one scalar node per multiply)."""
+    if not isinstance(node, BinaryElem) or node.kind not in (BinaryKind.plus, BinaryKind.minus):
+        return None
+    for prod_side, add_side, sign in ((node.left, node.right, 1.0), (node.right, node.left, None)):
+        mm, s2 = _scaled(prod_side)
+        if not isinstance(mm, MatMul):
+            continue
+        leaf, sb = _scaled(add_side)
+        if not isinstance(leaf, Leaf) or leaf.shape != mm.shape or leaf.etype is not mm.etype:
+            continue
+        if mm.etype not in (ElemType.f32, ElemType.f64):
+            continue
+        if node.kind is BinaryKind.plus:
+            return mm, s2, leaf, sb
+        # minus: left - right
+        if sign is not None:            # (s2*AB) - sb*C
+            return mm, s2, leaf, -sb
+        return mm, -s2, leaf, sb        # sb*C - s2*AB
+    return None
+
+
 def plan(out_mat_id: int, node: ExprNode) -> ExecutionPlan:
     """Plan `out = node` (`plan.py:171-205` semantics plus folding)."""
     p = _Planner()
     unsafe = aliases(out_mat_id, node) is AliasKind.UNSAFE
+
+    # s * (A @ B) at the root: the scale joins the product's epilogue
+    inner, s_root = _scaled(node)
+    if isinstance(inner, MatMul) and inner is not node and inner.etype in (ElemType.f32, ElemType.f64):
+        unsafe_mm = aliases(out_mat_id, inner) is AliasKind.UNSAFE
+        target = p.temp(inner.shape, inner.etype).temp_id if unsafe_mm else out_mat_id
+        step = p.gemm(inner, target)
+        step.alpha *= s_root            # one scale on the accumulator (the reference rounds T first)
+        return ExecutionPlan(p.steps, p.temps, target, inner.shape, inner.etype, out_is_temp=unsafe_mm)
+
+    ep = _product_epilogue(node)
+    if ep is not None:
+        mm, s2, c_leaf, beta = ep
+        # the product's operands must not alias the output; the addend may (read then written
+        # by the same thread)
+        if aliases(out_mat_id, mm) is not AliasKind.UNSAFE:
+            step = p.gemm(mm, out_mat_id)
+            step.c_id, step.alpha2, step.beta = c_leaf.mat_id, s2, beta
+            return ExecutionPlan(p.steps, p.temps, out_mat_id, node.shape, node.etype)
 
     if isinstance(node, MatMul):
         target = p.temp(node.shape, node.etype).temp_id if unsafe else out_mat_id

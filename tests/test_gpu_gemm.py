@@ -140,3 +140,57 @@ def test_c5_f32_size_sampled(gpu_ctx):
     cols = np.sort(rng.choice(n, 32, replace=False))
     x, y, z = X.to_numpy(), Y.to_numpy(), Z.to_numpy()
     _check(z[np.ix_(rows, cols)], x[rows, :], y[cols, :].T, 2.0)
+
+
+# --- GEMM epilogue fusion: s2*(A@B) +/- sb*C in one launch ---------------------------
+def _epilogue_cases():
+    return [("2*(A@B)+C", lambda A, B, C: 2 * (A @ B) + C, lambda t, c: np.float32(2) * t + c),
+            ("C-A@B", lambda A, B, C: C - A @ B, lambda t, c: c - t),
+            ("A@B-3*C", lambda A, B, C: A @ B - 3 * C, lambda t, c: t - np.float32(3) * c)]
+
+
+@pytest.mark.parametrize("case", _epilogue_cases(), ids=lambda c: c[0])
+def test_gemm_epilogue_exact_path_bit_exact(gpu_ctx, case):
+    """Small f32 products take the exact kernel: T is the reference's
+    f64-accumulated product rounded to f32, then the reference's elementwise
+    step with per-op f32 rounding -- bit for bit, in ONE launch (the
+    reference plans a MatMulStep plus a fused copy)."""
+    _, build, ref = case
+    ctx = fm.Context(gpu_ctx.backend)
+    a, b, c = _f32((96, 80), 1), _f32((80, 72), 2), _f32((96, 72), 3)
+    A, B, C = (fm.from_array(v, ctx=ctx) for v in (a, b, c))
+    Z = fm.zeros(96, 72, ctx=ctx)
+    ctx.reset_counters()
+    Z.assign(build(A, B, C))
+    assert ctx.launches == 1
+    t = (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(Z.to_numpy(), ref(t, c))
+
+
+@pytest.mark.parametrize("etype", ["f32", "bf16"])
+def test_gemm_epilogue_tensor_path(gpu_ctx, etype):
+    ctx = fm.Context(gpu_ctx.backend)
+    m, n, k = 1024, 768, 1152
+    a = _bf16((m, k), 4) if etype == "bf16" else _f32((m, k), 4)
+    b = _bf16((k, n), 5) if etype == "bf16" else _f32((k, n), 5)
+    c = _f32((m, n), 6)
+    A, B = fm.from_array(a, etype=etype, ctx=ctx), fm.from_array(b, etype=etype, ctx=ctx)
+    C = fm.from_array(c, ctx=ctx)
+    Z = fm.zeros(m, n, ctx=ctx)
+    ctx.reset_counters()
+    Z.assign(2 * (A @ B) + C)
+    assert ctx.launches == 1
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    want = 2 * (a64 @ b64) + c
+    bound = 1e-5 * (2 * (np.abs(a64) @ np.abs(b64)) + np.abs(c)) + 1e-30
+    assert np.all(np.abs(Z.to_numpy() - want) <= bound)
+
+
+def test_gemm_epilogue_in_place_and_f64(gpu_ctx):
+    ctx = fm.Context(gpu_ctx.backend)
+    a, b, c = (np.random.default_rng(s).random(sh) for s, sh in ((7, (50, 40)), (8, (40, 30)), (9, (50, 30))))
+    A, B, C = (fm.from_array(v, ctx=ctx) for v in (a, b, c))     # f64
+    ctx.reset_counters()
+    C.assign(C + A @ B)                                          # addend aliases the output
+    assert ctx.launches == 1
+    assert np.allclose(C.to_numpy(), (a @ b) + c, rtol=1e-12, atol=0)
