@@ -177,3 +177,31 @@ def test_aot_registry_covers_the_configs():
               ast.schur(ast.minus(X64, Y64), Z64), ast.schur(X64, Y64)):
         assert ast.signature_of(n) in sigs
     assert len(hot_expressions()) == len(sigs)
+
+
+# --- host-path memoisation ---------------------------------------
+def test_plan_and_bind_memo():
+    from recording import launches, recording_backend
+    import paper_2604_22242_b200 as fm
+    from paper_2604_22242_b200.errors import BackendError
+    b = recording_backend()
+    ctx = fm.Context(b)
+    X, Y, Z = fm.Mat(64, 32, "f32", ctx), fm.Mat(64, 32, "f32", ctx), fm.Mat(64, 32, "f32", ctx)
+    e = 2 * (X % Y) + X
+    Z.assign(e)
+    p1 = ctx.plan_for(Z.mat_id, e.node)
+    Z.assign(e)
+    assert ctx.plan_for(Z.mat_id, e.node) is p1            # same expression object: memoised plan
+    progs = [a[1]._obj for a in launches(b, "fm_launch_copy")]
+    assert progs[0] is progs[1]                           # same arguments: bound program re-used
+    e2 = 2 * (X % Y) + X
+    assert ctx.plan_for(Z.mat_id, e2.node) is not p1      # a new tree plans afresh
+    X._realloc(X.shape)                                   # new buffer: re-bound
+    Z.assign(e)
+    assert launches(b, "fm_launch_copy")[-1][1]._obj is not progs[0]
+    old = Y.handle
+    b.free(old)
+    Y._set_handle(b.alloc(Y.etype, Y.n_elem))
+    k = ctx.cache.lookup(p1.steps[0].signature)
+    with pytest.raises(BackendError):                     # memo never bypasses the UAF check
+        b.launch(k, [Z.handle, 64, 32, X.handle, 64, 32, old, 64, 32, 2.0], (64, 32))
