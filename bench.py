@@ -133,16 +133,26 @@ class ClockSampler:
 
 
 class Dist:
+    """torchrun plumbing: one process per GPU, NCCL.  FMB200_DIST_BACKEND=gloo
+    with FMB200_SHARE_GPU=1 runs every rank on GPU 0 over gloo -- a
+    functional check of the N>1 path on a one-GPU box (timings meaningless)."""
+
     def __init__(self):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if os.environ.get("FMB200_SHARE_GPU") == "1":
+            self.local = 0
         self.pg = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
             torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{self.local}"))
+            backend = os.environ.get("FMB200_DIST_BACKEND", "nccl")
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device(f"cuda:{self.local}"))
+            else:
+                dist.init_process_group(backend)
             self.pg = dist
 
     def barrier(self):
@@ -971,7 +981,8 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
-    ap.add_argument("--n", type=int, default=0, help="override the per-GPU size")
+    ap.add_argument("--size", "--n", dest="n", type=int, default=0,
+                    help="override the per-GPU size (use --size under torchrun: its parser claims --n)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
