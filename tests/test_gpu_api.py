@@ -383,3 +383,26 @@ def test_graph_capture_replays_the_same_kernels(ctx):
     g.replay()
     assert orc.max_ulp(z.to_numpy(), np.float32(2) * (yv * yv) + yv) == 0
     g.close()
+
+
+def test_log_f32_sweep_vs_correctly_rounded(ctx):
+    """log_f (ops.cuh, table-driven) over a dense sweep of positive f32 bit
+    patterns (subnormals to FLT_MAX), every f32 within 2^-6 of 1, and the
+    specials, against log evaluated in f64 and rounded once."""
+    pos = np.arange(1, 0x7f7fffff, 61, dtype=np.uint32).view(np.float32)
+    near = np.arange(np.float32(1 - 2**-6).view(np.uint32), np.float32(1 + 2**-6).view(np.uint32),
+                     1, dtype=np.uint32).view(np.float32)
+    special = np.array([0.0, -0.0, -1.0, np.inf, -np.inf, np.nan, 1.0, 2.0, 0.5,
+                        np.float32(1.4e-45), np.float32(3.4028235e38)], np.float32)
+    x = np.concatenate([pos, near, special]).astype(np.float32)
+    X = fm.from_array(x.reshape(-1, 1), ctx=ctx)
+    Z = fm.zeros(len(x), 1, ctx=ctx)
+    Z.assign(fm.log(X))
+    got = Z.to_numpy().ravel()
+    with np.errstate(divide="ignore", invalid="ignore"):
+        want = np.log(x.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    ok = ~np.isnan(want)
+    assert orc.max_ulp(got[ok], want[ok]) <= 1
+    diff = np.count_nonzero(got[ok].view(np.uint32) != want[ok].view(np.uint32))
+    assert diff <= max(4, len(x) // 1_000_000), diff
