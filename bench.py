@@ -506,6 +506,57 @@ class C4:
         return run, byts, "port", 1, f"numpy restatement on {self.rows}x{cols}, 1 thread"
 
 
+class C4Rows(C4):
+    """C4's expression reduced along rows (dim 1): 65536-long row sums / means /
+    maxima / index_max over 16384 columns in one pass (column-split CTAs,
+    last-CTA combine in split order).  Not a BASELINE config: the row
+    variant of the same API, same algorithmic bytes."""
+    name = "c4r"
+    workload = ("C4-rows row-wise sum/mean/max/index_max of (X - Y) % Z, f64 65536x16384 per GPU, one fused "
+                "multi-output pass")
+
+    def __init__(self, args, d):
+        super().__init__(args, d)
+        self.labels = ["c4_rowstats_f64"]
+        self.kbytes = [3 * 8 * self.rows * self.cols + 3 * 8 * self.rows + 4 * self.rows]
+
+    def setup(self, fm, ctx):
+        super().setup(fm, ctx)
+        r = self.rows
+        self.outs = [fm.Mat(r, 1, "f64", ctx), fm.Mat(r, 1, "f64", ctx), fm.Mat(r, 1, "f64", ctx),
+                     fm.Mat(r, 1, "u32", ctx)]
+
+    def launches(self):
+        fm, e, o = self.fm, self.e, self.outs
+        return [lambda: fm.assign_all([(o[0], fm.sum(e, 1)), (o[1], fm.mean(e, 1)),
+                                       (o[2], fm.max(e, 1)), (o[3], fm.index_max(e, 1))])]
+
+    def check(self):
+        from oracle import fm_oracle as orc
+        rows = slice(0, 64)
+        sub = lambda M: M.to_numpy()[rows, :]  # noqa: E731
+        v = (sub(self.X) - sub(self.Y)) * sub(self.Z)
+        k = orc.ReduceKind
+        return {"index_max_exact_64_rows": bool(np.array_equal(
+                    self.outs[3].to_numpy()[rows, :], orc.reduce_dim(k.index_max, 1, v, orc.ElemType.f64))),
+                "sum_rel_err_64_rows": orc.compare(self.outs[0].to_numpy()[rows, :],
+                                                   orc.reduce_dim(k.sum, 1, v, orc.ElemType.f64))}
+
+    def cpu(self, n_sample, threads):
+        from oracle import fm_oracle as orc
+        cols = max(1, n_sample // self.rows)
+        X = orc.randu(self.rows, cols, 42, "f64")
+        Y = orc.randu(self.rows, cols, 43, "f64")
+        Z = orc.randu(self.rows, cols, 44, "f64")
+        byts = 3 * 8 * self.rows * cols
+
+        def run():
+            v = (X - Y) * Z
+            k = orc.ReduceKind
+            return [orc.reduce_dim(kk, 1, v, orc.ElemType.f64) for kk in (k.sum, k.mean, k.max, k.index_max)]
+        return run, byts, "port", 1, f"numpy restatement on {self.rows}x{cols}, 1 thread"
+
+
 class C5:
     """Z = 2 * X @ Y.t(), bf16 operands, f32 result, 8192^3: one tcgen05 launch
     (the reference plans it as 2 materialising copies + a naive GEMM)."""
@@ -739,7 +790,7 @@ def plan_bytes(pl) -> int:
     return total
 
 
-CONFIGS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "c5": C5, "c5f32": C5F32, "suite": Suite}
+CONFIGS = {"c1": C1, "c2": C2, "c3": C3, "c4": C4, "c4r": C4Rows, "c5": C5, "c5f32": C5F32, "suite": Suite}
 
 
 # --------------------------------------------------------------------------------------
@@ -760,7 +811,7 @@ def time_cpu(run, byts, steps, warmup, scale=1e9):
 
 def cpu_sample_elems(cfg_name: str) -> int:
     return {"c2": 20_000_000, "c1": 4096 * 4096, "c3": 4096 * 4096, "c4": 65536 * 64,
-            "c5": 2048 ** 3, "c5f32": 2048 ** 3, "suite": 4096 * 4096}[cfg_name]
+            "c4r": 65536 * 64, "c5": 2048 ** 3, "c5f32": 2048 ** 3, "suite": 4096 * 4096}[cfg_name]
 
 
 def reference_arm(args, d: Dist):

@@ -560,7 +560,54 @@ __global__ void __launch_bounds__(kThreads) k_reduce_rows(const __grid_constant_
   Stats s[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) stats_init(s[v]);
-  if (active) {
+  bool done_fast = false;
+  if constexpr (E::kFast) {
+    // Typed fast path: whole V-row runs of a flat, 16-byte aligned program.
+    // The next column's vectors are loaded while the current one is folded
+    // into branch-free per-row stats (columns visited in increasing order, so
+    // a strictly-better test keeps the first index).
+    using T = typename E::Elem;
+    constexpr int NIN = E::kNin, kW = E::kW, NQ = V / kW;
+    if (active && cnt == V && E::fast_ok(P, nullptr) && ((n_rows * (int64_t)sizeof(T)) & 15) == 0 &&
+        n_cols < 0xFFFFFFFFll) {
+      ColStats<T> cs[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) cs[v].init();
+      uint4 cur[NIN][NQ], nxt[NIN][NQ];
+      auto load = [&](int64_t col, uint4 (&b)[NIN][NQ]) {
+#pragma unroll
+        for (int i = 0; i < NIN; ++i) {
+          const T *p = (const T *)P.slots[i].ptr + col * n_rows + row0;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) b[i][q] = ldg_v4(p + q * kW);
+        }
+      };
+      if (c0 < c1) load(c0, cur);
+      for (int64_t col = c0; col < c1; ++col) {
+        if (col + 1 < c1) load(col + 1, nxt);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+          for (int e = 0; e < kW; ++e) {
+            T x[NIN];
+#pragma unroll
+            for (int i = 0; i < NIN; ++i) {
+              if constexpr (sizeof(T) == 8) x[i] = e == 0 ? u2d(cur[i][q].x, cur[i][q].y) : u2d(cur[i][q].z, cur[i][q].w);
+              else x[i] = u2f(e == 0 ? cur[i][q].x : e == 1 ? cur[i][q].y : e == 2 ? cur[i][q].z : cur[i][q].w);
+            }
+            cs[q * kW + e].add(E::ev_elem(P, x), (uint32_t)col, need);
+          }
+#pragma unroll
+        for (int i = 0; i < NIN; ++i)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) cur[i][q] = nxt[i][q];
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) cs[v].to_stats(s[v]);
+      done_fast = true;
+    }
+  }
+  if (active && !done_fast) {
     for (int64_t col = c0; col < c1; ++col) {
       Chunk ch;
       ch.row0 = row0; ch.col = col; ch.base = row0 + col * n_rows; ch.cnt = cnt;

@@ -145,3 +145,29 @@ def test_bulk_staged_copy_beyond_l2(ctx, etype):
     x, y = X.to_numpy(), Y.to_numpy()
     t = x.dtype.type(2)
     assert np.array_equal(Z.to_numpy(), t * (x * y) + x)
+
+
+@pytest.mark.parametrize("etype", ["f32", "f64"])
+def test_row_stats_fast_path_nan_and_ties(ctx, etype):
+    """dim-1 reductions on the typed fast path (whole V-row runs, columns in
+    increasing order within each column split, splits combined in order):
+    ties and NaNs placed in different splits, plus a ragged last row run."""
+    rows, cols = 64 + 2, 5000
+    rng = np.random.default_rng(7)
+    a = rng.integers(-3, 4, size=(rows, cols)).astype(np.float32 if etype == "f32" else np.float64)
+    a[1, :] = 7.0                      # all equal: column 0 wins
+    a[2, 4000] = 50.0
+    a[2, 100] = 50.0                   # tie across splits: first column (100)
+    a[3, 2500] = np.nan
+    a[3, 4100] = np.nan                # first NaN wins
+    a[65, 4999] = 99.0                 # the ragged row run
+    a[5, :] = -np.inf
+    X = fm.from_array(a, ctx=ctx)
+    ety = fm.ElemType.of(etype)
+    for fn, kind in ((fm.max, orc.ReduceKind.max), (fm.index_max, orc.ReduceKind.index_max),
+                     (fm.min, orc.ReduceKind.min), (fm.index_min, orc.ReduceKind.index_min)):
+        got = fn(X, 1).eval().to_numpy()
+        want = orc.reduce_dim(kind, 1, a, ety)
+        assert np.array_equal(got, want, equal_nan=True), (fn.__name__,)
+    got = fm.sum(X, 1).eval().to_numpy()
+    assert orc.compare(got, orc.reduce_dim(orc.ReduceKind.sum, 1, a, ety)) < 1e-12
