@@ -17,6 +17,7 @@ import math
 from pathlib import Path
 
 from . import exprtree as ast
+from . import lower as lw
 from .exprtree import ElemType, MatShape
 
 _S = MatShape(4, 4)
@@ -193,7 +194,8 @@ def generate(path: Path) -> Path:
         typ, nin, ety = cpp_type(node)
         T = "float" if ety is ElemType.f32 else "double"
         V = vector_width(nin, ety)
-        full = f"TEval<{typ}, {T}, {nin}, {V}>"
+        tiled = not lw.lower(node).flat       # transposed / view leaves
+        full = f"TEval<{typ}, {T}, {nin}, {V}, {'true' if tiled else 'false'}>"
         lines.append(f"// {label}: {sig}")
         if full not in types:
             i = types[full] = len(types)

@@ -137,7 +137,9 @@ int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cud
   // flat many-leaf programs on the VM, staging measured slower -- add8N 3.5
   // -> 1.6 TB/s, the VM's per-instruction cost dominates -- so the add-N
   // chains get AOT templates instead)
-  if (tiled_enabled() && !P.flat && n_rows * n_cols >= 4096) return run_copy_tiled<E>(P, out, n_rows, n_cols, s);
+  if constexpr (E::kTiled) {
+    if (tiled_enabled() && !P.flat && n_rows * n_cols >= 4096) return run_copy_tiled<E>(P, out, n_rows, n_cols, s);
+  }
   if constexpr (E::kFast) {
     if constexpr (bulk::Geometry<E>::kOk) {
       const int64_t n = n_rows * n_cols;
@@ -220,7 +222,13 @@ int run_reduce_dim(const fm_program &P, int dim, int64_t n_rows, int64_t n_cols,
   }
   const int64_t gx = cdiv(n_rows, (int64_t)kThreads * V);
   if (gx > 65535 * 1024LL) return fail_msg("reduce_dim: too many rows");
-  int64_t splits = std::max<int64_t>(1, cdiv((int64_t)sm_count() * 4, gx));
+  static const int64_t per_sm = [] {
+    const char *e = getenv("FMB200_ROW_SPLITS_PER_SM");
+    return (int64_t)((e && *e) ? std::max(1, atoi(e)) : 16);
+  }();
+  // column splits so ~16 CTAs per SM stream concurrently (c4r, 65536 x 16384
+  // f64: 2 -> 4.74, 4 -> 5.80, 8 -> 6.13, 16 -> 6.37, 32 -> 5.95 TB/s)
+  int64_t splits = std::max<int64_t>(1, cdiv((int64_t)sm_count() * per_sm, gx));
   splits = std::min<int64_t>(splits, std::min<int64_t>(n_cols, 65535));
   RowPartial *part = nullptr;
   unsigned *counters = nullptr;

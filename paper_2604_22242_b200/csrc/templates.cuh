@@ -114,8 +114,11 @@ template <class A, class B> struct RegTiles<Mul<A, B>> { static constexpr bool v
 // chunks); the *_tile members serve the steady state of a flat program whose
 // buffers are all 16-byte aligned: typed 128-bit loads and stores with no
 // per-element type dispatch or bounds checks.
-template <class Expr, class T, int NIN, int V>
+template <class Expr, class T, int NIN, int V, bool TILED = false>
 struct TEval {
+  // TILED: the signature has transposed / view leaves, so copies run on the
+  // tiled staged skeleton (instantiated only for those templates)
+  static constexpr bool kTiled = TILED;
   using Elem = T;
   static constexpr int kV = V;
   static constexpr int kNin = NIN;

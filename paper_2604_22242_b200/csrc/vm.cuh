@@ -189,6 +189,7 @@ struct Vm {
   static constexpr int kV = V;
   static constexpr bool kWide = WIDE;
   static constexpr bool kIsVm = true;
+  static constexpr bool kTiled = true;
   static constexpr bool kFast = false;
   FM_DEV static bool fast_ok(const fm_program &, const void *) { return false; }
   static constexpr int HD = WIDE ? MAXD : 1;
