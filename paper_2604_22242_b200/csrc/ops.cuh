@@ -217,7 +217,37 @@ __device__ __forceinline__ float log_f(float a) {
   if (a == __int_as_float(0x7f800000)) res = a;
   return res;
 }
-__device__ __forceinline__ float tanh_f(float a) { return __double2float_rn(tanh((double)a)); }
+// tanh of an f32 argument, correctly rounded in practice (f64 evaluation,
+// one rounding): tanh|x| = m / (m + 2) with m = expm1(2|x|) from the same
+// 64-entry exp table (2^(j/64) * (1 + p) - 1: absolute error ~2^-53, relative
+// <= 2^-41 for 2|x| >= 2^-11) and a correctly rounded f64 reciprocal; ~24
+// FP64 operations instead of libdevice tanh's branchy rational forms (the
+// paper's gelu).  |x| < 2^-12 returns x (tanh x = x(1 - x^2/3 + ...) rounds
+// to x); |x| >= 9.1 returns +-1 (1 - tanh|x| < 2^-25).
+__device__ __forceinline__ float tanh_f(float a) {
+  const float ax = fabsf(a);
+  const double y = 2.0 * (double)fminf(ax, 9.5f);
+  const double kMagic = 0x1.8p52;
+  const double t = fma(y, 0x1.71547652b82fep+6, kMagic);   // rint(y*64/ln2) + 1.5*2^52
+  const double n = __dsub_rn(t, kMagic);
+  const int ni = __double2loint(t);
+  double r = fma(-n, 0x1.62e42fee00000p-7, y);
+  r = fma(-n, 0x1.a39ef35793c76p-39, r);
+  double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  const double p = __dmul_rn(q, r);                         // exp(r) - 1
+  const double tj = __ldg(&kExp2Tab64[ni & 63]);
+  const double sc = __hiloint2double(__double2hiint(tj) + (int)((unsigned)(ni >> 6) << 20), __double2loint(tj));
+  const double m = fma(sc, p, __dsub_rn(sc, 1.0));          // 2^(n/64) (1 + p) - 1
+  const double th = __dmul_rn(m, __drcp_rn(__dadd_rn(m, 2.0)));
+  float res = __double2float_rn(th);
+  if (ax < 0x1p-12f) res = ax;
+  if (ax >= 9.1f) res = 1.0f;
+  res = copysignf(res, a);
+  return (a != a) ? a : res;
+}
 __device__ __forceinline__ double exp_d(double a) { return exp(a); }
 __device__ __forceinline__ double log_d(double a) { return log(a); }
 __device__ __forceinline__ double tanh_d(double a) { return tanh(a); }

@@ -406,3 +406,27 @@ def test_log_f32_sweep_vs_correctly_rounded(ctx):
     assert orc.max_ulp(got[ok], want[ok]) <= 1
     diff = np.count_nonzero(got[ok].view(np.uint32) != want[ok].view(np.uint32))
     assert diff <= max(4, len(x) // 1_000_000), diff
+
+
+def test_tanh_f32_sweep_vs_correctly_rounded(ctx):
+    """tanh_f (ops.cuh, expm1 from the exp table + f64 reciprocal) over a
+    dense sweep of f32 bit patterns in [-10, 10], the small-argument and
+    saturation boundaries, and the specials."""
+    pos = np.arange(0, np.float32(10.0).view(np.uint32), 53, dtype=np.uint32).view(np.float32)
+    edges = np.concatenate([np.arange(np.float32(2**-13).view(np.uint32), np.float32(2**-11).view(np.uint32),
+                                      97, dtype=np.uint32).view(np.float32),
+                            np.arange(np.float32(8.9).view(np.uint32), np.float32(9.3).view(np.uint32),
+                                      1, dtype=np.uint32).view(np.float32)])
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-30, 20.0, 88.0], np.float32)
+    x = np.concatenate([pos, -pos, edges, -edges, special]).astype(np.float32)
+    X = fm.from_array(x.reshape(-1, 1), ctx=ctx)
+    Z = fm.zeros(len(x), 1, ctx=ctx)
+    Z.assign(fm.tanh(X))
+    got = Z.to_numpy().ravel()
+    want = np.tanh(x.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    ok = ~np.isnan(want)
+    assert orc.max_ulp(got[ok], want[ok]) <= 1
+    assert np.array_equal(np.signbit(got[ok]), np.signbit(want[ok]))     # tanh(-0) = -0
+    diff = np.count_nonzero(got[ok].view(np.uint32) != want[ok].view(np.uint32))
+    assert diff <= max(4, len(x) // 1_000_000), diff
