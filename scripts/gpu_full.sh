@@ -10,7 +10,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1
 timeout 600 python bench.py --impl reference > gpurun_out/bench_reference.log 2>&1
-for c in ${CONFIGS:-c1 c3 c4 c5 c5f32 suite}; do
+for c in ${CONFIGS:-c1 c3 c4 c4r c5 c5f32 suite}; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/bench_$c.log 2>&1
 done
 if [ -z "$NO_LAUNCHES" ]; then

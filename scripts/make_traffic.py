@@ -23,6 +23,7 @@ LABELS = {
     "norm_sqdiff_f64": "ncu_c2_norm_f64",
     "c3_copy_f32": "ncu_c3_copy",
     "c4_colstats_f64": "ncu_c4_colstats",
+    "c4_rowstats_f64": "ncu_c4r_rowstats",
     "c5_gemm_bf16": "ncu_c5_gemm",
     "c5_gemm_f32": "ncu_c5f32_gemm",
     "expr1": "ncu_suite_expr1",
