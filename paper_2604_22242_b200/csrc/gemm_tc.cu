@@ -348,6 +348,246 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   }
 }
 
+// ---- CTA-pair (cta_group::2) variant ---------------------------------------------------
+// A cluster of two CTAs on one TPC computes a 256 x 256 tile: each CTA TMA-
+// loads its own 128-row half of A and 128-column half of B (32 KiB per stage
+// instead of 48, so 6 stages fit), the leader (rank 0) issues
+// tcgen05.mma.cta_group::2 (M=256, N=256) that reads both CTAs' shared
+// memory, and each CTA's TMEM holds the accumulator rows of its half.  Both
+// CTAs' TMA completions count on the leader's full barrier; MMA commits are
+// multicast to both CTAs' empty / tfull barriers; both epilogues report a
+// drained accumulator to the leader's tempty barrier.
+namespace pair {
+constexpr int BM2 = 256, BNH = 128;                  // pair tile 256 x 256, per-CTA B half 128
+constexpr int A_BYTES2 = 128 * BK * 2;               // 16 KiB (this CTA's rows)
+constexpr int B_BYTES2 = BNH * BK * 2;               // 16 KiB (this CTA's columns)
+constexpr int STAGE_BYTES2 = A_BYTES2 + B_BYTES2;
+constexpr int STAGES2 = 7;
+constexpr int SMEM_BYTES2 = STAGES2 * STAGE_BYTES2 + 1024 + 256;
+constexpr int BN2 = 256;                             // accumulator columns per CTA
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (a shared::cta address in this CTA) in CTA `rank`
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *map, uint32_t leader_bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__host__ __device__ constexpr uint32_t make_idesc_pair(bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(BM2 >> 4) << 24);
+}
+}  // namespace pair
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTc, 1)
+    k_gemm_bf16_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                     const Params p) {
+  using namespace pair;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(smem + STAGES2 * STAGE_BYTES2);
+  uint64_t *empty = full + STAGES2;
+  uint64_t *tfull = empty + STAGES2;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_holder = (uint32_t *)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int ntm = (p.m + BM2 - 1) / BM2, ntn = (p.n + BN2 - 1) / BN2;
+  const int ntiles = ntm * ntn;
+  const int nv = p.nprod * p.nkb;
+  const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kEpiWarps);   // both CTAs' epilogue warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const uint32_t leader_full0 = mapa(smem_u32(&full[0]), 0);
+  const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs): this CTA's A rows and B columns; bytes count on the leader's barrier
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair_id; t < ntiles; t += npairs) {
+        int mb, nb;
+        tile_coords(t, ntm, ntn, mb, nb);
+        const int m0 = mb * BM2 + 128 * (int)rank, n0 = nb * BN2 + BNH * (int)rank;
+        int prod = 0, kb = 0;
+        for (int v = 0; v < nv; ++v, ++kb) {
+          if (kb == p.nkb) { kb = 0; ++prod; }
+          const int ka = (int)((p.pa >> (3 * prod)) & 7u) * p.kplane + kb * BK;
+          const int kbb = (int)((p.pb >> (3 * prod)) & 7u) * p.kplane + kb * BK;
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *sa = smem + stage * STAGE_BYTES2;
+          uint8_t *sb = sa + A_BYTES2;
+          const uint32_t lbar = leader_full0 + (uint32_t)(stage * 8);
+          if (leader) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES2);
+          if (p.a_mn) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) tma_load_2d_pair(sa + j * (64 * BK * 2), &map_a, lbar, m0 + 64 * j, ka);
+          } else {
+            tma_load_2d_pair(sa, &map_a, lbar, ka, m0);
+          }
+          if (p.b_mn) {
+#pragma unroll
+            for (int j = 0; j < BNH / 64; ++j) tma_load_2d_pair(sb + j * (64 * BK * 2), &map_b, lbar, n0 + 64 * j, kbb);
+          } else {
+            tma_load_2d_pair(sb, &map_b, lbar, kbb, n0);
+          }
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer: leader only
+    if (leader) {
+      const uint32_t idesc = make_idesc_pair(p.a_mn != 0, p.b_mn != 0);
+      const uint32_t a_step = p.a_mn ? 2048u : 32u, b_step = p.b_mn ? 2048u : 32u;
+      const uint32_t a_lbo = p.a_mn ? 64u * BK * 2 : 16u, b_lbo = p.b_mn ? 64u * BK * 2 : 16u;
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t gc = 0;
+      for (int t = pair_id; t < ntiles; t += npairs) {
+        for (int v0 = 0; v0 < nv; v0 += p.kc, ++gc) {
+          const int acc = (int)(gc & 1u);
+          const uint32_t use = gc >> 1;
+          mbar_wait(&tempty[acc], (use & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN2);
+          const int vend = min(nv, v0 + p.kc);
+          for (int v = v0; v < vend; ++v) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (lane == 0) {
+              const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES2);
+              const uint32_t sb = sa + A_BYTES2;
+#pragma unroll
+              for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                const uint64_t ad = make_desc(sa + kk * a_step, a_lbo, 1024u);
+                const uint64_t bd = make_desc(sb + kk * b_step, b_lbo, 1024u);
+                umma_bf16_pair(d_tmem, ad, bd, idesc, (v != v0 || kk != 0) ? 1u : 0u);
+              }
+              umma_commit_pair(&empty[stage]);                   // frees the slot in BOTH CTAs
+              if (v == vend - 1) umma_commit_pair(&tfull[acc]);  // accumulator halves ready in both CTAs
+            }
+            __syncwarp();
+            if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else {
+    // ===== epilogue (both CTAs): this CTA's 128 accumulator rows
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    uint32_t gc = 0;
+    for (int t = pair_id; t < ntiles; t += npairs) {
+      int mb, nb;
+      tile_coords(t, ntm, ntn, mb, nb);
+      float sum[BN2 / 2];
+#pragma unroll
+      for (int j = 0; j < BN2 / 2; ++j) sum[j] = 0.0f;
+      for (int v0 = 0; v0 < nv; v0 += p.kc, ++gc) {
+        const int acc = (int)(gc & 1u);
+        const uint32_t use = gc >> 1;
+        mbar_wait(&tfull[acc], use & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN2 + h * (BN2 / 2));
+#pragma unroll
+        for (int c4 = 0; c4 < BN2 / 64; ++c4) {
+          uint32_t vv[32];
+          tmem_ld32_nowait(taddr + c4 * 32, vv);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sum[c4 * 32 + j] = __fadd_rn(sum[c4 * 32 + j], __uint_as_float(vv[j]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_tempty0 + (uint32_t)(acc * 8));
+      }
+      const int row = mb * BM2 + 128 * (int)rank + q * 32 + lane;
+      if (row < p.m) {
+        float *cp = p.c + row;
+        const int col0 = nb * BN2 + h * (BN2 / 2);
+        if (p.cin) {
+          const float *ci = p.cin + row;
+#pragma unroll
+          for (int j = 0; j < BN2 / 2; ++j)
+            if (col0 + j < p.n) {
+              const float tt = __fmul_rn(p.alpha, sum[j]);
+              cp[(int64_t)(col0 + j) * p.ldc] =
+                  __fadd_rn(__fmul_rn(p.alpha2, tt), __fmul_rn(p.beta, ci[(int64_t)(col0 + j) * p.ldcin]));
+            }
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN2 / 2; ++j)
+            if (col0 + j < p.n) cp[(int64_t)(col0 + j) * p.ldc] = p.alpha * sum[j];
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
 // f32 -> three bf16 planes with x = hi + mid + lo + O(2^-24 |x|): each
 // residual is exact in f32 (Sterbenz), each plane the round-to-nearest bf16
 // of the residual.  Plane p of element (i, j) goes to out[p*plane_off + i + j*ld_out].
@@ -474,6 +714,15 @@ int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
   p.a_mn = g.trans_a ? 0 : 1;   // op(A) = A (m x k, M-contiguous) or A^T of a k x m buffer (K-contiguous)
   p.b_mn = g.trans_b ? 1 : 0;   // op(B) = B (k x n, K-contiguous) or B^T of an n x k buffer (N-contiguous)
   p.nkb = (int)((g.k + BK - 1) / BK);
+  // CTA-pair kernel (cta_group::2, 256 x 256 pair tiles) by default: C5 1441
+  // vs 1405 TF/s on the single-CTA kernel.  FMB200_GEMM_PAIR=0 selects the
+  // single-CTA kernel (A/B measurements).
+  static int pair_env = [] {
+    const char *e = getenv("FMB200_GEMM_PAIR");
+    return (e && *e) ? atoi(e) : 1;
+  }();
+  const bool use_pair = pair_env == 1 && sm_count() >= 2;
+  const int b_box_rows = use_pair ? pair::BNH : BN;   // K-major B box: this CTA's columns
   static int kc_env = [] {
     const char *e = getenv("FMB200_GEMM_KC");
     return (e && *e) ? std::max(1, atoi(e)) : KC;
@@ -497,7 +746,7 @@ int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
                 : split_operand((const float *)g.b, g.k, g.n, g.ldb, false, kplane, &pb, s);
     if (st) { cudaFreeAsync(pa.buf, s); return st; }
     st = encode_map(&ma, pa.buf, pa.inner, pa.outer, pa.ld, p.a_mn ? 64 : BK, p.a_mn ? BK : BM);
-    if (!st) st = encode_map(&mb, pb.buf, pb.inner, pb.outer, pb.ld, p.b_mn ? 64 : BK, p.b_mn ? BK : BN);
+    if (!st) st = encode_map(&mb, pb.buf, pb.inner, pb.outer, pb.ld, p.b_mn ? 64 : BK, p.b_mn ? BK : b_box_rows);
   } else {
     p.nprod = 1;
     p.kplane = 0;
@@ -506,8 +755,29 @@ int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
     else st = encode_map(&ma, g.a, (uint64_t)g.k, (uint64_t)g.m, (uint64_t)g.lda, BK, BM);
     if (!st) {
       if (p.b_mn) st = encode_map(&mb, g.b, (uint64_t)g.n, (uint64_t)g.k, (uint64_t)g.ldb, 64, BK);
-      else st = encode_map(&mb, g.b, (uint64_t)g.k, (uint64_t)g.n, (uint64_t)g.ldb, BK, BN);
+      else st = encode_map(&mb, g.b, (uint64_t)g.k, (uint64_t)g.n, (uint64_t)g.ldb, BK, b_box_rows);
     }
+  }
+  if (!st && use_pair) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaError_t e = cudaFuncSetAttribute(k_gemm_bf16_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           pair::SMEM_BYTES2);
+      if (e != cudaSuccess) st = fail("cudaFuncSetAttribute(k_gemm_bf16_pair)", e);
+      else attr2 = true;
+    }
+    if (!st) {
+      const int ntiles = (int)(((g.m + pair::BM2 - 1) / pair::BM2) * ((g.n + pair::BN2 - 1) / pair::BN2));
+      const int grid = std::min(2 * ntiles, sm_count() & ~1);
+      k_gemm_bf16_pair<<<grid, kThreadsTc, pair::SMEM_BYTES2, s>>>(ma, mb, p);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) st = fail("tcgen05 gemm kernel (CTA pair)", e);
+      else count_launch();
+    }
+    if (pa.buf) cudaFreeAsync(pa.buf, s);
+    if (pb.buf) cudaFreeAsync(pb.buf, s);
+    if (!st) *handled = true;
+    return st;
   }
   if (!st) {
     static bool attr_set = false;
