@@ -60,8 +60,10 @@ int get_scratch(void *stream, size_t payload_bytes, Scratch *out) {
   ScratchEntry &e = g_scratch[{dev, stream}];
   cudaStream_t s = (cudaStream_t)stream;
   if (e.base == nullptr || e.payload < payload_bytes) {
+    // grow geometrically; the outgrown block is retired, not freed, because a
+    // CUDA graph captured earlier (fm_graph_*) may still hold its address
     size_t want = payload_bytes < (size_t)(1 << 20) ? (size_t)(1 << 20) : payload_bytes;
-    if (e.base) FM_CHECK(cudaFreeAsync(e.base, s));
+    if (want < 2 * e.payload) want = 2 * e.payload;
     FM_CHECK(cudaMallocAsync(&e.base, kCounterBytes + want, s));
     FM_CHECK(cudaMemsetAsync(e.base, 0, kCounterBytes, s));
     e.payload = want;
