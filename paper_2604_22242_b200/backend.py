@@ -381,7 +381,6 @@ class B200Backend(Backend):
             tmpl.slots[j].transposed = int(s.transposed)
         # schema positions (codegen.py:304-318 order)
         in_pos, view_pos, scalar_pos = [], [], []
-        pos = 3 if skeleton != REDUCE_DIM else 3
         roles = [a.role for a in schema]
         p = 3
         while p < len(roles) and roles[p] == "in":
