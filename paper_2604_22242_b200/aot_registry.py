@@ -73,6 +73,12 @@ def hot_expressions() -> list[tuple[str, ast.ExprNode]]:
         out.append((f"expr2_{t}", ast.plus(ast.plus(ast.scalar_pre_mul(2.0, X),
                                                     ast.transpose(ast.plus(Y, Z))),
                                            ast.log(ast.pow_int(W, 2)))))
+        # expr3 (bench.py:141-145): 1 / (x % conv_to(u, T) + log(log(x + 2) % w)), u a u32 leaf
+        U = ast.leaf(1, ElemType.u32, _B)
+        W3 = ast.leaf(2, ety, _B)
+        out.append((f"expr3_{t}", ast.scalar_pre_div(1, ast.plus(
+            ast.schur(X, ast.conv(U, ety)),
+            ast.log(ast.schur(ast.log(ast.scalar_add(X, 2)), W3))))))
         d = [ast.diag(i, ety, k, _B) for i, k in ((0, -1), (0, 1), (1, -1), (1, 1))]
         out.append((f"diagsum_{t}", ast.schur(ast.plus(d[0], d[1]), ast.plus(d[2], d[3]))))
     # the paper's add-N sweep (reference bench.py:307-326, Fig. 5):
@@ -129,6 +135,11 @@ def cpp_type(node: ast.ExprNode) -> tuple[str, int, ElemType]:
         return slots.setdefault((i, kind, tr, v), len(slots))
 
     def go(n, tr=False) -> str:
+        if (isinstance(n, ast.UnaryElem) and n.kind is ast.UnaryKind.conv and n.target is ety
+                and isinstance(n.child, ast.Leaf) and n.child.etype in (ElemType.u32, ElemType.i32)):
+            # an integer leaf converted to the template type (paper expr3)
+            kind = "CvtU32" if n.child.etype is ElemType.u32 else "CvtI32"
+            return f"{kind}<{leaf_slot(n.child, tr)}>"
         if n.etype is not ety:
             raise ValueError("templates need a single element type")
         if isinstance(n, (ast.Leaf, ast.Subview, ast.Diag)):

@@ -48,6 +48,13 @@ template <int S, class A> struct SAdd { FM_EV { return tadd(A::ev(x, s), scal<T>
 template <int S, class A> struct SMul { FM_EV { return tmul(scal<T>(s[S]), A::ev(x, s)); } };
 template <int S, class A> struct SDiv { FM_EV { return tdiv(scal<T>(s[S]), A::ev(x, s)); } };
 template <int S, class A> struct Gts { FM_EV { return tgt(A::ev(x, s), scal<T>(s[S])); } };
+// conversion of an integer leaf (slot I holds u32 / i32 bits) to T, as the
+// reference's C cast (codegen.py:217-218): round to nearest
+template <class T> FM_DEV uint32_t leaf_bits(T v);
+template <> FM_DEV uint32_t leaf_bits<float>(float v) { return __float_as_uint(v); }
+template <> FM_DEV uint32_t leaf_bits<double>(double v) { return (uint32_t)__double2loint(v); }
+template <int I> struct CvtU32 { FM_EV { return (T)leaf_bits<T>(x[I]); } };
+template <int I> struct CvtI32 { FM_EV { return (T)(int32_t)leaf_bits<T>(x[I]); } };
 template <class A> struct Neg { FM_EV { return tneg(A::ev(x, s)); } };
 template <class A> struct Abs { FM_EV { return tabs(A::ev(x, s)); } };
 template <class A> struct Exp { FM_EV { return texp(A::ev(x, s)); } };
