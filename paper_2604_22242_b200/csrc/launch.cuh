@@ -61,7 +61,9 @@ template <class E>
 bool host_fast_ok(const fm_program &P, const void *out) {
   if (!P.flat || P.result_etype != E::kEtype || (((uintptr_t)out) & 15)) return false;
   for (int i = 0; i < P.n_slots; ++i)
-    if ((((uintptr_t)P.slots[i].ptr) & 15) || P.slots[i].etype != E::kEtype) return false;
+    if ((((uintptr_t)P.slots[i].ptr) & 15) || !(P.slots[i].etype == E::kEtype ||
+        (sizeof(typename E::Elem) == 4 && (P.slots[i].etype == FM_U32 || P.slots[i].etype == FM_I32))))
+      return false;
   return true;
 }
 

@@ -162,11 +162,16 @@ struct TEval {
   }
 
   // uniform per launch: may the tile members run?
+  // a slot the tile paths can move as T-sized words: T itself, or (f32
+  // templates) the u32 / i32 leaf of a CvtU32 / CvtI32 node
+  FM_DEV static constexpr bool slot_ok(int et) {
+    return et == kEtype || (sizeof(T) == 4 && (et == FM_U32 || et == FM_I32));
+  }
   FM_DEV static bool fast_ok(const fm_program &P, const void *out) {
     if (!P.flat || P.result_etype != kEtype || (((uintptr_t)out) & 15)) return false;
 #pragma unroll
     for (int i = 0; i < NIN; ++i)
-      if ((((uintptr_t)P.slots[i].ptr) & 15) || P.slots[i].etype != kEtype) return false;
+      if ((((uintptr_t)P.slots[i].ptr) & 15) || !slot_ok(P.slots[i].etype)) return false;
     return true;
   }
 
