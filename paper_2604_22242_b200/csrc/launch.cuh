@@ -140,7 +140,11 @@ int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cud
   // -> 1.6 TB/s, the VM's per-instruction cost dominates -- so the add-N
   // chains get AOT templates instead)
   if constexpr (E::kTiled) {
-    if (tiled_enabled() && !P.flat && n_rows * n_cols >= 4096) return run_copy_tiled<E>(P, out, n_rows, n_cols, s);
+    // transposed leaves need the staged tile; views alone read their column
+    // runs directly (vector loads in load_slot)
+    bool transposed = false;
+    for (int j = 0; j < P.n_slots; ++j) transposed |= P.slots[j].transposed != 0;
+    if (tiled_enabled() && transposed && n_rows * n_cols >= 4096) return run_copy_tiled<E>(P, out, n_rows, n_cols, s);
   }
   if constexpr (E::kFast) {
     if constexpr (bulk::Geometry<E>::kOk) {

@@ -124,7 +124,7 @@ constexpr int kCopyDepth() {
 }
 
 template <class E>
-__global__ void __launch_bounds__(kThreads) k_copy(const __grid_constant__ fm_program P, void *out,
+__global__ void __launch_bounds__(kThreads, E::kMinBlocks) k_copy(const __grid_constant__ fm_program P, void *out,
                                                    int64_t n_rows, int64_t n_cols) {
   constexpr int V = E::kV;
   pdl_trigger();

@@ -133,6 +133,9 @@ struct TEval {
   // inputs; wider chains (add-N) load all inputs of a chunk at once instead
   static constexpr bool kFast = NIN <= 8;
   static constexpr bool kIsVm = false;
+  // the widest chains (add-N, N > 16) hold NIN x V loaded words per thread:
+  // ask for two resident blocks so they keep 16 warps per SM
+  static constexpr int kMinBlocks = NIN > 16 ? 2 : 1;
   static constexpr bool kWide = sizeof(T) == 8;
   static constexpr bool kHeavy = Heavy<Expr>::v;
   static constexpr bool kRegTiles = RegTiles<Expr>::v;
@@ -146,7 +149,7 @@ struct TEval {
   FM_DEV static void eval(const fm_program &P, const Chunk &ch, uint32_t (&lo)[V], uint32_t (&hi)[V]) {
     uint32_t xl[NIN][V], xh[NIN][V];
 #pragma unroll
-    for (int i = 0; i < NIN; ++i) fetch_slot<V>(P, i, ch, xl[i], xh[i]);
+    for (int i = 0; i < NIN; ++i) fetch_slot<V, !TILED>(P, i, ch, xl[i], xh[i]);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       T xv[NIN];

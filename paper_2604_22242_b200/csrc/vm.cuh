@@ -67,14 +67,73 @@ struct Chunk {
   int slot_bytes = 0;        // bytes per staged slot
 };
 
+// Load V elements of slot s for a flat chunk (every slot dense, same shape).
+template <int V>
+FM_DEV void load_slot_flat(const fm_slot &s, const Chunk &ch, uint32_t (&lo)[V], uint32_t (&hi)[V]);
+
+template <int V>
+FM_DEV void load_slot_flat(const fm_slot &s, const Chunk &ch, uint32_t (&lo)[V], uint32_t (&hi)[V]) {
+  const int64_t b = ch.base;
+  if (s.etype == FM_F64) {
+    const unsigned long long *p = (const unsigned long long *)s.ptr + b;
+    if (ch.cnt == V && (((uintptr_t)p) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < V / 2; ++q) {
+        uint4 w = ldg_v4(p + 2 * q);
+        lo[2 * q] = w.x; hi[2 * q] = w.y; lo[2 * q + 1] = w.z; hi[2 * q + 1] = w.w;
+      }
+      return;
+    }
+  } else if (s.etype == FM_BF16) {
+    const uint16_t *p = (const uint16_t *)s.ptr + b;
+    if (ch.cnt == V && (((uintptr_t)p) & (2 * V - 1)) == 0 && (V == 4 || V == 8)) {
+      if (V == 8) {
+        uint4 w = ldg_v4(p);
+        uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4 && 2 * q + 1 < V; ++q) {
+          lo[2 * q] = ws[q] << 16; lo[2 * q + 1] = ws[q] & 0xffff0000u;
+        }
+      } else {
+        uint2 w = ldg_v2(p);
+        lo[0] = w.x << 16; lo[1] = w.x & 0xffff0000u;
+        lo[2 % V] = w.y << 16; lo[3 % V] = w.y & 0xffff0000u;
+      }
+      return;
+    }
+  } else {
+    const uint32_t *p = (const uint32_t *)s.ptr + b;
+    if (ch.cnt == V && (((uintptr_t)p) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < V / 4; ++q) {
+        uint4 w = ldg_v4(p + 4 * q);
+        lo[4 * q] = w.x; lo[4 * q + 1] = w.y; lo[4 * q + 2] = w.z; lo[4 * q + 3] = w.w;
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    lo[v] = 0; hi[v] = 0;
+    if (v < ch.cnt) load_one(s, b + v, lo[v], hi[v]);
+  }
+  return;
+}
+
 // Load V elements of slot s for the chunk.
 template <int V>
 FM_DEV void load_slot(const fm_slot &s, const Chunk &ch, uint32_t (&lo)[V], uint32_t (&hi)[V]) {
   if (ch.flat) {
-    const int64_t b = ch.base;
-    if (s.etype == FM_F64) {
-      const unsigned long long *p = (const unsigned long long *)s.ptr + b;
-      if (ch.cnt == V && (((uintptr_t)p) & 15) == 0) {
+    load_slot_flat<V>(s, ch, lo, hi);
+    return;
+  }
+  // untransposed dense / subview leaf: the chunk's V rows are consecutive in
+  // one parent column -- vector loads when the run is whole and aligned
+  if (!s.transposed && s.map != FM_MAP_DIAG && ch.cnt == V) {
+    const int64_t i0 = slot_index(s, ch.row0, ch.col);
+    if (s.etype == FM_F64 && V % 2 == 0) {
+      const unsigned long long *p = (const unsigned long long *)s.ptr + i0;
+      if ((((uintptr_t)p) & 15) == 0) {
 #pragma unroll
         for (int q = 0; q < V / 2; ++q) {
           uint4 w = ldg_v4(p + 2 * q);
@@ -82,26 +141,9 @@ FM_DEV void load_slot(const fm_slot &s, const Chunk &ch, uint32_t (&lo)[V], uint
         }
         return;
       }
-    } else if (s.etype == FM_BF16) {
-      const uint16_t *p = (const uint16_t *)s.ptr + b;
-      if (ch.cnt == V && (((uintptr_t)p) & (2 * V - 1)) == 0 && (V == 4 || V == 8)) {
-        if (V == 8) {
-          uint4 w = ldg_v4(p);
-          uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int q = 0; q < 4 && 2 * q + 1 < V; ++q) {
-            lo[2 * q] = ws[q] << 16; lo[2 * q + 1] = ws[q] & 0xffff0000u;
-          }
-        } else {
-          uint2 w = ldg_v2(p);
-          lo[0] = w.x << 16; lo[1] = w.x & 0xffff0000u;
-          lo[2 % V] = w.y << 16; lo[3 % V] = w.y & 0xffff0000u;
-        }
-        return;
-      }
-    } else {
-      const uint32_t *p = (const uint32_t *)s.ptr + b;
-      if (ch.cnt == V && (((uintptr_t)p) & 15) == 0) {
+    } else if (s.etype != FM_F64 && s.etype != FM_BF16 && V % 4 == 0) {
+      const uint32_t *p = (const uint32_t *)s.ptr + i0;
+      if ((((uintptr_t)p) & 15) == 0) {
 #pragma unroll
         for (int q = 0; q < V / 4; ++q) {
           uint4 w = ldg_v4(p + 4 * q);
@@ -110,12 +152,6 @@ FM_DEV void load_slot(const fm_slot &s, const Chunk &ch, uint32_t (&lo)[V], uint
         return;
       }
     }
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      lo[v] = 0; hi[v] = 0;
-      if (v < ch.cnt) load_one(s, b + v, lo[v], hi[v]);
-    }
-    return;
   }
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -174,11 +210,17 @@ FM_DEV void load_staged(const fm_slot &s, const unsigned char *buf, const Chunk 
 
 // Slot j of the program for the chunk: staged tile when the kernel staged it
 // (every slot but diagonals), global memory otherwise.
-template <int V>
+template <int V, bool FLAT_ONLY = false>
 FM_DEV void fetch_slot(const fm_program &P, int j, const Chunk &ch, uint32_t (&lo)[V], uint32_t (&hi)[V]) {
   const fm_slot &s = P.slots[j];
-  if (ch.stage && s.map != FM_MAP_DIAG) load_staged<V>(s, ch.stage + (size_t)j * ch.slot_bytes, ch, lo, hi);
-  else load_slot<V>(s, ch, lo, hi);
+  if constexpr (FLAT_ONLY) {
+    // evaluators whose programs are always flat (flat-signature templates)
+    // carry no view / staging code: fewer live registers
+    load_slot_flat<V>(s, ch, lo, hi);
+  } else {
+    if (ch.stage && s.map != FM_MAP_DIAG) load_staged<V>(s, ch.stage + (size_t)j * ch.slot_bytes, ch, lo, hi);
+    else load_slot<V>(s, ch, lo, hi);
+  }
 }
 
 // -----------------------------------------------------------------------------
@@ -189,6 +231,7 @@ struct Vm {
   static constexpr int kV = V;
   static constexpr bool kWide = WIDE;
   static constexpr bool kIsVm = true;
+  static constexpr int kMinBlocks = 1;
   static constexpr bool kTiled = true;
   static constexpr bool kFast = false;
   FM_DEV static bool fast_ok(const fm_program &, const void *) { return false; }
