@@ -220,6 +220,23 @@ int run_reduce_dim(const fm_program &P, int dim, int64_t n_rows, int64_t n_cols,
     return 0;
   }
   if (dim == 0) {
+    if constexpr (E::kFast) {
+      using T = typename E::Elem;
+      if (host_fast_ok<E>(P, nullptr) && ((n_rows * (int64_t)sizeof(T)) & 15) == 0 && n_rows % E::kTile == 0 &&
+          n_rows < 0xFFFFFFFFll) {
+        // 3 CTAs per SM (C4, 65536 x 16384 f64: 2 -> 7.01, 3 -> 7.38, 4 -> 7.23,
+        // 6 -> 7.24 TB/s); FMB200_COLS_BLOCKS_PER_SM overrides
+        static const int per_sm = [] {
+          const char *e = getenv("FMB200_COLS_BLOCKS_PER_SM");
+          return (e && *e) ? std::max(1, atoi(e)) : 3;
+        }();
+        const int64_t grid = std::min<int64_t>(std::min<int64_t>(n_cols, (int64_t)sm_count() * per_sm),
+                                               wave_grid<GridTag<E, 4>>(k_reduce_cols_fast<E>, n_cols));
+        FM_CHECK(launch_pdl(k_reduce_cols_fast<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, P, R, n_rows, n_cols));
+        FM_CHECK_LAUNCH("fused column-reduction kernel (typed)");
+        return 0;
+      }
+    }
     // one persistent wave; columns are the work units (C4: 16384 / 444)
     const int64_t grid = wave_grid<GridTag<E, 2>>(k_reduce_cols<E>, n_cols);
     FM_CHECK(launch_pdl(k_reduce_cols<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, P, R, n_rows, n_cols));

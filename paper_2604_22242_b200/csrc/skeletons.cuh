@@ -450,6 +450,26 @@ struct ColStats {
   }
 };
 
+// General chunk path of a column (ragged row remainder, or programs without
+// the typed fast path).  Out of line so its register needs do not crowd the
+// fast path's loop in the same kernel.
+template <class E>
+__device__ __noinline__ void cols_generic(const fm_program &P, Stats &s, int64_t col, int64_t row_start,
+                                          int64_t n_rows, int rt, bool fl, unsigned need) {
+  constexpr int V = E::kV;
+  for (int64_t row0 = row_start + (int64_t)threadIdx.x * V; row0 < n_rows; row0 += (int64_t)kThreads * V) {
+    Chunk ch;
+    ch.row0 = row0; ch.col = col; ch.base = row0 + col * n_rows;
+    ch.cnt = (int)min((int64_t)V, n_rows - row0);
+    ch.flat = P.flat != 0;
+    uint32_t lo[V], hi[V];
+    E::eval(P, ch, lo, hi);
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (v < ch.cnt) stats_add(s, rt, fl, lo[v], hi[v], row0 + v, need);
+  }
+}
+
 // dim 0: one block per column (grid-stride over columns).  Fast path (typed
 // evaluator, flat program, 16-byte aligned columns): each warp streams warp
 // tiles of its column with the next tile's loads in flight while the current
@@ -506,17 +526,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_reduce_cols(const __grid_consta
         row_start = fast_rows;
       }
     }
-    for (int64_t row0 = row_start + (int64_t)threadIdx.x * V; row0 < n_rows; row0 += (int64_t)kThreads * V) {
-      Chunk ch;
-      ch.row0 = row0; ch.col = col; ch.base = row0 + col * n_rows;
-      ch.cnt = (int)min((int64_t)V, n_rows - row0);
-      ch.flat = P.flat != 0;
-      uint32_t lo[V], hi[V];
-      E::eval(P, ch, lo, hi);
-#pragma unroll
-      for (int v = 0; v < V; ++v)
-        if (v < ch.cnt) stats_add(s, rt, fl, lo[v], hi[v], row0 + v, need);
-    }
+    if (row_start < n_rows) cols_generic<E>(P, s, col, row_start, n_rows, rt, fl, need);
     Stats t = s;
     if (need & 1u) {
       t.sum = block_sum_d(s.sum, smd);
@@ -526,6 +536,58 @@ __global__ void __launch_bounds__(kThreads, 3) k_reduce_cols(const __grid_consta
     if (need & 4u) t.mn = block_best<false>(s.mn, smc);
     if (threadIdx.x == 0)
       for (int i = 0; i < R.n; ++i) emit_out(R.o[i], col, t, rt, fl, n_rows);
+    __syncthreads();
+  }
+}
+
+// dim 0, typed fast path only: every column is a whole number of warp tiles
+// (the host checks).  A kernel of its own so that no general-path code shares
+// its register allocation (measured: with the chunk path in the same kernel
+// ptxas spilled inside this loop, C4 7.46 -> 7.10 TB/s).
+template <class E>
+__global__ void __launch_bounds__(kThreads, 3) k_reduce_cols_fast(const __grid_constant__ fm_program P,
+                                                               const __grid_constant__ ReduceOuts R,
+                                                               int64_t n_rows, int64_t n_cols) {
+  constexpr int V = E::kV;
+  using T = typename E::Elem;
+  constexpr int kTile = E::kTile, kW = E::kW;
+  __shared__ double smd[kThreads / 32];
+  __shared__ uint32_t smu[kThreads / 32];
+  __shared__ Cand smc[kThreads / 32];
+  const int rt = P.result_etype;
+  const unsigned need = needed_stats(R);
+  pdl_trigger();
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t ntile = n_rows / kTile;
+  for (int64_t col = blockIdx.x; col < n_cols; col += gridDim.x) {
+    Stats s;
+    stats_init(s);
+    const int64_t cbase = col * n_rows;
+    ColStats<T> cs;
+    cs.init();
+    int64_t t = threadIdx.x >> 5;
+    typename E::Buf buf;
+    if (t < ntile) E::load_tile(P, cbase + t * kTile, lane, buf);
+    for (; t < ntile; t += kThreads / 32) {
+      const typename E::Buf cur = buf;
+      if (t + kThreads / 32 < ntile) E::load_tile(P, cbase + (t + kThreads / 32) * kTile, lane, buf);
+      T r[V];
+      E::eval_tile(P, cur, r);
+      const uint32_t r0 = (uint32_t)(t * kTile) + lane * kW;
+#pragma unroll
+      for (int q = 0; q < V / kW; ++q)
+#pragma unroll
+        for (int e = 0; e < kW; ++e) cs.add(r[q * kW + e], r0 + q * 32 * kW + e, need);
+    }
+    cs.to_stats(s);
+    Stats tt = s;
+    if (need & 1u) tt.sum = block_sum_d(s.sum, smd);
+    if (need & 2u) tt.mx = block_best<true>(s.mx, smc);
+    if (need & 4u) tt.mn = block_best<false>(s.mn, smc);
+    (void)smu;
+    if (threadIdx.x == 0)
+      for (int i = 0; i < R.n; ++i) emit_out(R.o[i], col, tt, rt, true, n_rows);
     __syncthreads();
   }
 }
