@@ -94,19 +94,21 @@ def test_c4_full_size_sampled(ctx):
     assert np.array_equal(got[3], orc.reduce_dim(k.index_max, 0, v, f64))
 
 
+@pytest.mark.parametrize("rows", [4096 + 24, 4096])
 @pytest.mark.parametrize("etype", ["f32", "f64"])
-def test_column_stats_fast_path_nan_and_ties(ctx, etype):
+def test_column_stats_fast_path_nan_and_ties(ctx, etype, rows):
     """Ties and NaNs at rows owned by different warps / tiles of the typed
-    fast path (tiles of 32*V rows), plus a ragged remainder."""
-    rows, cols = 4096 + 24, 9
+    fast path (tiles of 32*V rows), with a ragged remainder (general kernel
+    finishing the column) and without one (the typed-only kernel)."""
+    cols = 9
     rng = np.random.default_rng(5)
     a = rng.integers(-3, 4, size=(rows, cols)).astype(np.float32 if etype == "f32" else np.float64)
     a[:, 1] = 7.0                      # all equal: index 0 wins
     a[3000, 2] = 50.0
     a[100, 2] = 50.0                   # tie across tiles: first index (100)
     a[2500, 3] = np.nan
-    a[4100, 3] = np.nan                # first NaN wins max / index_max (2500)
-    a[4100, 4] = 99.0                  # maximum in the ragged remainder
+    a[rows - 1, 3] = np.nan            # first NaN wins max / index_max (2500)
+    a[rows - 1, 4] = 99.0              # maximum in the last rows
     a[:, 5] = -np.inf
     a[17, 6] = np.inf
     X = fm.from_array(a, ctx=ctx)
