@@ -174,7 +174,11 @@ int run_accu_bulk(const fm_program &P, void *out, int64_t n_elem, int finalize, 
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, sm_count()));
   // static head: 80 % of the chunks round-robin (summed per CTA), the rest
   // claimed dynamically with one partial slot each
-  const int64_t nstat = chunks * 4 / 5 / grid;
+  static const int64_t static_pct = [] {
+    const char *e = getenv("FMB200_BULK_STATIC_PCT");
+    return (int64_t)((e && *e) ? std::min(100, std::max(0, atoi(e))) : 80);
+  }();
+  const int64_t nstat = chunks * static_pct / 100 / grid;
   const int64_t ndyn = chunks - nstat * grid;
   Scratch sc;
   int st = get_scratch((void *)s, (grid + ndyn) * sizeof(double) + 64, &sc);
