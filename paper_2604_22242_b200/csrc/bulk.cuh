@@ -76,7 +76,7 @@ template <class E>
 struct Geometry {
   using T = typename E::Elem;
   static constexpr int kNin = E::kNin;
-  static constexpr int kChunkBytes = kNin <= 4 ? kChunkBytesMax : kChunkBytesMax / 2;
+  static constexpr int kChunkBytes = kNin <= 2 ? 2 * kChunkBytesMax : (kNin <= 4 ? kChunkBytesMax : kChunkBytesMax / 2);
   static constexpr int kChunk = kChunkBytes / (int)sizeof(T);               // elements per chunk
   static constexpr int kStagesRaw = kSmemBudget / (kChunkBytes * (kNin > 0 ? kNin : 1));
   static constexpr int kStages = kStagesRaw > 8 ? 8 : (kStagesRaw < 2 ? 2 : kStagesRaw);
