@@ -166,13 +166,14 @@ struct Params {
   const float *cin; // epilogue addend (nullptr: none)
   int64_t ldcin;
   float alpha2, beta;
+  int group_m;      // M-blocks per rasterisation group (L2 reuse of B)
 };
 
-__device__ __forceinline__ void tile_coords(int t, int ntm, int ntn, int &mb, int &nb) {
-  const int per_group = GROUP_M * ntn;
+__device__ __forceinline__ void tile_coords(int t, int ntm, int ntn, int &mb, int &nb, int group_m = GROUP_M) {
+  const int per_group = group_m * ntn;
   const int g = t / per_group;
-  const int first = g * GROUP_M;
-  const int gsize = min(GROUP_M, ntm - first);
+  const int first = g * group_m;
+  const int gsize = min(group_m, ntm - first);
   const int r = t - g * per_group;
   mb = first + r % gsize;
   nb = r / gsize;
@@ -463,7 +464,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTc, 1)
       uint32_t phase = 0;
       for (int t = pair_id; t < ntiles; t += npairs) {
         int mb, nb;
-        tile_coords(t, ntm, ntn, mb, nb);
+        tile_coords(t, ntm, ntn, mb, nb, p.group_m);
         const int m0 = mb * BM2 + 128 * (int)rank, n0 = nb * BN2 + BNH * (int)rank;
         int prod = 0, kb = 0;
         for (int v = 0; v < nv; ++v, ++kb) {
@@ -536,7 +537,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTc, 1)
     uint32_t gc = 0;
     for (int t = pair_id; t < ntiles; t += npairs) {
       int mb, nb;
-      tile_coords(t, ntm, ntn, mb, nb);
+      tile_coords(t, ntm, ntn, mb, nb, p.group_m);
       float sum[BN2 / 2];
 #pragma unroll
       for (int j = 0; j < BN2 / 2; ++j) sum[j] = 0.0f;
@@ -728,6 +729,11 @@ int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
     return (e && *e) ? std::max(1, atoi(e)) : KC;
   }();
   p.kc = kc_env;
+  static int group_env = [] {
+    const char *e = getenv("FMB200_GEMM_GROUP_M");
+    return (e && *e) ? std::max(1, atoi(e)) : GROUP_M;
+  }();
+  p.group_m = group_env;
   CUtensorMap ma, mb;
   int st;
   Planes pa, pb;
