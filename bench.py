@@ -1041,7 +1041,7 @@ def main(argv=None):
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
-    d = Dist() if args.impl == "ours" or int(os.environ.get("WORLD_SIZE", "1")) > 1 else Dist()
+    d = Dist()
     try:
         if args.impl == "reference":
             return reference_arm(args, d)
