@@ -51,7 +51,7 @@ struct Geo {
   static constexpr int TRP = TR + 8;             // column-major pitch: 16-byte column starts for w = 2, 4, 8
   static constexpr int TCP = TC;                 // row-major pitch (16-byte chunks swizzled, see stage_tile)
   static constexpr int LTR = V == 8 ? 6 : (V == 4 ? 5 : 4);   // log2(TR)
-  static constexpr int LTC = TC == 32 ? 5 : (TC == 16 ? 4 : 3);
+  static constexpr int LTC = TC == 64 ? 6 : (TC == 32 ? 5 : (TC == 16 ? 4 : 3));
   static constexpr int SB0 = (TC * TRP > TR * TCP ? TC * TRP : TR * TCP) * WMAX;
   static constexpr int SLOT_BYTES = (SB0 + 15) / 16 * 16;
 };
@@ -115,9 +115,30 @@ FM_DEV void stage_tile(const fm_program &P, unsigned char *buf, int64_t r0, int6
   }
 }
 
+// Tile t -> (row block, column block).  Paired order (square tiles on a
+// square grid): tiles (I,J) and (J,I) are consecutive, so CTAs running at the
+// same time stage both -- the block a transposed leaf reads for (I,J) is the
+// block the untransposed leaf of the same matrix reads for (J,I), and the
+// second read hits L2 instead of HBM.  Group J holds (0,J),(J,0),(1,J),(J,1),
+// ..., (J,J); it starts at tile J^2.
+FM_DEV void tile_of(int64_t t, int64_t ntr, bool paired, int64_t &bi, int64_t &bj) {
+  if (!paired) {
+    bi = t % ntr;
+    bj = t / ntr;
+    return;
+  }
+  int64_t J = (int64_t)sqrt((double)t);
+  while (J * J > t) --J;
+  while ((J + 1) * (J + 1) <= t) ++J;
+  const int64_t u = t - J * J;
+  if (u == 2 * J) { bi = J; bj = J; return; }
+  const int64_t I = u >> 1;
+  if (u & 1) { bi = J; bj = I; } else { bi = I; bj = J; }
+}
+
 template <class E, int TC>
 __global__ void __launch_bounds__(8 * TC) k_copy_tiled(const __grid_constant__ fm_program P, void *out,
-                                                        int64_t n_rows, int64_t n_cols) {
+                                                        int64_t n_rows, int64_t n_cols, int paired) {
   constexpr int V = E::kV, WMAX = E::kWide ? 8 : 4;
   using G = Geo<V, TC, WMAX>;
   extern __shared__ __align__(16) unsigned char sm[];
@@ -127,21 +148,27 @@ __global__ void __launch_bounds__(8 * TC) k_copy_tiled(const __grid_constant__ f
   const int k = threadIdx.x & 7, cc = threadIdx.x >> 3;
   int64_t t = blockIdx.x;
   if (t < ntiles) {
-    const int64_t r0 = (t % ntr) * G::TR, c0 = (t / ntr) * TC;
+    int64_t bi, bj;
+    tile_of(t, ntr, paired != 0, bi, bj);
+    const int64_t r0 = bi * G::TR, c0 = bj * TC;
     stage_tile<V, TC, WMAX>(P, sm, r0, c0, (int)min((int64_t)G::TR, n_rows - r0), (int)min((int64_t)TC, n_cols - c0));
   }
   cp_commit();
   for (int b = 0; t < ntiles; t += gridDim.x, b ^= 1) {
     const int64_t tn = t + gridDim.x;
     if (tn < ntiles) {
-      const int64_t r0 = (tn % ntr) * G::TR, c0 = (tn / ntr) * TC;
+      int64_t bi, bj;
+      tile_of(tn, ntr, paired != 0, bi, bj);
+      const int64_t r0 = bi * G::TR, c0 = bj * TC;
       stage_tile<V, TC, WMAX>(P, sm + (b ^ 1) * buf_bytes, r0, c0, (int)min((int64_t)G::TR, n_rows - r0),
                         (int)min((int64_t)TC, n_cols - c0));
     }
     cp_commit();
     cp_wait<1>();        // this tile's copies (all but the newest group) have landed
     __syncthreads();
-    const int64_t r0 = (t % ntr) * G::TR, c0 = (t / ntr) * TC;
+    int64_t bi, bj;
+    tile_of(t, ntr, paired != 0, bi, bj);
+    const int64_t r0 = bi * G::TR, c0 = bj * TC;
     const int rv = (int)min((int64_t)G::TR, n_rows - r0), cv = (int)min((int64_t)TC, n_cols - c0);
     if (cc < cv && k * V < rv) {
       Chunk ch;
