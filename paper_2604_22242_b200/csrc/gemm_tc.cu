@@ -592,21 +592,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTc, 1)
 // f32 -> three bf16 planes with x = hi + mid + lo + O(2^-24 |x|): each
 // residual is exact in f32 (Sterbenz), each plane the round-to-nearest bf16
 // of the residual.  Plane p of element (i, j) goes to out[p*plane_off + i + j*ld_out].
+__device__ __forceinline__ void split3(float x, uint16_t &h, uint16_t &m, uint16_t &l) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+  const float r1 = __fsub_rn(x, __bfloat162float(hi));
+  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+  const float r2 = __fsub_rn(r1, __bfloat162float(mid));
+  h = __bfloat16_as_ushort(hi);
+  m = __bfloat16_as_ushort(mid);
+  l = __bfloat16_as_ushort(__float2bfloat16_rn(r2));
+}
+
+// Grid: x over row runs of 4 elements, y over columns (no per-element
+// division); 16-byte loads and 8-byte stores per plane when the column runs
+// are aligned, scalar otherwise.
 __global__ void k_split3(const float *__restrict__ in, int64_t rows, int64_t cols, int64_t ld_in,
                          uint16_t *__restrict__ out, int64_t ld_out, int64_t plane_off) {
-  const int64_t n = rows * cols;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / rows, i = e - j * rows;
-    const float x = in[i + j * ld_in];
-    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-    const float r1 = __fsub_rn(x, __bfloat162float(hi));
-    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-    const float r2 = __fsub_rn(r1, __bfloat162float(mid));
-    const __nv_bfloat16 lo = __float2bfloat16_rn(r2);
-    const int64_t o = i + j * ld_out;
-    out[o] = __bfloat16_as_ushort(hi);
-    out[o + plane_off] = __bfloat16_as_ushort(mid);
-    out[o + 2 * plane_off] = __bfloat16_as_ushort(lo);
+  const bool vec = ((ld_in & 3) == 0) && ((ld_out & 3) == 0) && ((plane_off & 3) == 0) &&
+                   ((((uintptr_t)in) & 15) == 0) && ((((uintptr_t)out) & 7) == 0);
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    const float *src = in + j * ld_in;
+    uint16_t *dst = out + j * ld_out;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x * 4) {
+      if (vec && i + 4 <= rows) {
+        const float4 x = *(const float4 *)(src + i);
+        ushort4 h, m, l;
+        split3(x.x, h.x, m.x, l.x);
+        split3(x.y, h.y, m.y, l.y);
+        split3(x.z, h.z, m.z, l.z);
+        split3(x.w, h.w, m.w, l.w);
+        *(ushort4 *)(dst + i) = h;
+        *(ushort4 *)(dst + i + plane_off) = m;
+        *(ushort4 *)(dst + i + 2 * plane_off) = l;
+      } else {
+        for (int64_t ii = i; ii < i + 4 && ii < rows; ++ii) {
+          uint16_t h, m, l;
+          split3(src[ii], h, m, l);
+          dst[ii] = h;
+          dst[ii + plane_off] = m;
+          dst[ii + 2 * plane_off] = l;
+        }
+      }
+    }
   }
 }
 
@@ -691,9 +718,9 @@ int split_operand(const float *src, int64_t rows, int64_t cols, int64_t ld_in, b
   FM_CHECK(cudaMallocAsync((void **)&pl->buf, (size_t)bytes, s));
   const int64_t kdim = k_is_cols ? cols : rows;
   if (kdim != kplane) FM_CHECK(cudaMemsetAsync(pl->buf, 0, (size_t)bytes, s));   // zero K padding
-  const int64_t n = rows * cols;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8));
-  tc::k_split3<<<(unsigned)grid, 256, 0, s>>>(src, rows, cols, ld_in, pl->buf, ld_out, plane_off);
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 1023) / 1024, 64));
+  const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cols, 65535));
+  tc::k_split3<<<dim3(gx, gy), 256, 0, s>>>(src, rows, cols, ld_in, pl->buf, ld_out, plane_off);
   FM_CHECK_LAUNCH("f32 -> bf16 plane split kernel");
   return 0;
 }
