@@ -592,6 +592,24 @@ __global__ void __launch_bounds__(kThreads, 3) k_reduce_cols_fast(const __grid_c
   }
 }
 
+// General chunk path of a row run over columns [c0, c1): out of line so the
+// typed fast path keeps its registers (as cols_generic).
+template <class E>
+__device__ __noinline__ void rows_generic(const fm_program &P, Stats (&s)[E::kV], int64_t row0, int cnt,
+                                          int64_t c0, int64_t c1, int64_t n_rows, int rt, bool fl, unsigned need) {
+  constexpr int V = E::kV;
+  for (int64_t col = c0; col < c1; ++col) {
+    Chunk ch;
+    ch.row0 = row0; ch.col = col; ch.base = row0 + col * n_rows; ch.cnt = cnt;
+    ch.flat = P.flat != 0;
+    uint32_t lo[V], hi[V];
+    E::eval(P, ch, lo, hi);
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (v < cnt) stats_add(s[v], rt, fl, lo[v], hi[v], col, need);
+  }
+}
+
 // dim 1: each thread owns V consecutive rows; blockIdx.y splits the columns.
 // With several splits, partial stats go to scratch and the last block of each
 // row tile combines them in split order (one launch, deterministic).
@@ -669,18 +687,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_rows(const __grid_constant_
       done_fast = true;
     }
   }
-  if (active && !done_fast) {
-    for (int64_t col = c0; col < c1; ++col) {
-      Chunk ch;
-      ch.row0 = row0; ch.col = col; ch.base = row0 + col * n_rows; ch.cnt = cnt;
-      ch.flat = P.flat != 0;
-      uint32_t lo[V], hi[V];
-      E::eval(P, ch, lo, hi);
-#pragma unroll
-      for (int v = 0; v < V; ++v)
-        if (v < cnt) stats_add(s[v], rt, fl, lo[v], hi[v], col, need);
-    }
-  }
+  if (active && !done_fast) rows_generic<E>(P, s, row0, cnt, c0, c1, n_rows, rt, fl, need);
   if (splits == 1) {
     if (active)
 #pragma unroll
