@@ -194,3 +194,36 @@ def test_gemm_epilogue_in_place_and_f64(gpu_ctx):
     C.assign(C + A @ B)                                          # addend aliases the output
     assert ctx.launches == 1
     assert np.allclose(C.to_numpy(), (a @ b) + c, rtol=1e-12, atol=0)
+
+
+def test_gemm_epilogue_with_folded_transposes(gpu_ctx):
+    """Scale, transposes and the addend all fold into one launch:
+    3 * (X.t() @ Y.t()) - C with X, Y stored untransposed (tensor path)."""
+    ctx = fm.Context(gpu_ctx.backend)
+    m, n, k = 640, 384, 896
+    x = _f32((k, m), 11)            # X.t() is m x k
+    y = _f32((n, k), 12)            # Y.t() is k x n
+    c = _f32((m, n), 13)
+    X, Y, C = (fm.from_array(v, ctx=ctx) for v in (x, y, c))
+    Z = fm.zeros(m, n, ctx=ctx)
+    ctx.reset_counters()
+    Z.assign(3 * (X.t() @ Y.t()) - C)
+    assert ctx.launches == 1
+    a64, b64 = x.T.astype(np.float64), y.T.astype(np.float64)
+    want = 3 * (a64 @ b64) - c
+    bound = 1e-5 * (3 * (np.abs(a64) @ np.abs(b64)) + np.abs(c)) + 1e-30
+    assert np.all(np.abs(Z.to_numpy() - want) <= bound)
+
+
+def test_accu_of_transposed_and_view_expressions(gpu_ctx):
+    """Full reductions over non-flat programs (transposed / view leaves)."""
+    ctx = fm.Context(gpu_ctx.backend)
+    X = fm.randu(700, 700, 21, "f64", ctx)
+    Y = fm.randu(700, 700, 22, "f64", ctx)
+    x, y = X.to_numpy(), Y.to_numpy()
+    got = fm.accu(X.t() % Y)
+    want = orc.accu(x.T * y, orc.ElemType.f64)
+    assert abs(got - want) <= 1e-12 * abs(want)
+    got = fm.accu(X.submat(5, 7, 300, 200) - Y.submat(1, 2, 300, 200))
+    want = orc.accu(x[5:305, 7:207] - y[1:301, 2:202], orc.ElemType.f64)
+    assert abs(got - want) <= 1e-12 * max(1.0, abs(want))
