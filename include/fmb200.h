@@ -223,6 +223,11 @@ int fm_graph_begin(void *stream);
 int fm_graph_end(void *stream, void **graph, int64_t *kernels);
 int fm_graph_launch(void *graph, void *stream);
 int fm_graph_destroy(void *graph);
+/* Buffers allocated or freed while a thread captures (between fm_graph_begin
+ * and fm_graph_end) are owned by the graph: plain allocations, released only
+ * once every graph that captured them is destroyed and the owner freed them.
+ * Returns how many such buffers are currently alive (tests). */
+int64_t fm_graph_owned_count(void);
 
 /* number of kernels this library launched since load (for bench gpu_launches) */
 int64_t fm_launch_counter(void);

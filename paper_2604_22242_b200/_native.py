@@ -121,9 +121,11 @@ SIGNATURES = {
     "fm_graph_end": [_P, ctypes.POINTER(_P), ctypes.POINTER(_I64)],
     "fm_graph_launch": [_P, _P],
     "fm_graph_destroy": [_P],
+    "fm_graph_owned_count": [],
     "fm_launch_counter": [],
 }
-_RESTYPES = {"fm_last_error": ctypes.c_char_p, "fm_launch_counter": ctypes.c_int64}
+_RESTYPES = {"fm_last_error": ctypes.c_char_p, "fm_launch_counter": ctypes.c_int64,
+             "fm_graph_owned_count": ctypes.c_int64}
 
 
 class Native:

@@ -240,6 +240,7 @@ class B200Backend(Backend):
         self._freed: set[int] = set()
         self._next_id = 0
         self.launch_count = 0
+        self.closed = False
 
     @classmethod
     def available(cls) -> bool:
@@ -324,10 +325,7 @@ class B200Backend(Backend):
         data = np.ascontiguousarray(to_storage(flat, handle.etype))
         if data.size:
             self.nat.call("fm_memcpy_h2d", ptr, data.ctypes.data, data.nbytes, self.stream)
-            if not _is_pinned_view(data):
-                # pageable source: the copy is synchronous w.r.t. the host buffer
-                pass
-            self.synchronize()
+            self.synchronize()      # `data` may be a temporary: finish before it goes away
 
     def upload_async(self, host: np.ndarray, handle: BufferHandle) -> None:
         """H2D from a pinned, F-ordered, storage-typed host array without a
@@ -441,10 +439,10 @@ class B200Backend(Backend):
             raise SchemaError(f"geometry {geometry} != domain dims {(n_rows, n_cols)}")
         # the same arguments as the kernel's previous launch re-use its bound
         # program (buffers are re-checked for use-after-free)
-        key = tuple(args)
+        key = _memo_key(args)
         memo = getattr(kernel, "_memo", None)
         if memo is not None and memo[0] == key:
-            for a in key:
+            for a in args:
                 if isinstance(a, BufferHandle) and (a.id in self._freed or a.id not in self._ptrs):
                     raise BackendError(f"use after free of buffer {a.id}")
             prog = memo[1]
@@ -562,6 +560,7 @@ class B200Backend(Backend):
         self.launch_count += 1
 
     def close(self) -> None:
+        self.closed = True
         for hid, p in list(self._ptrs.items()):
             if hid not in self._views:
                 self.nat.call("fm_free", p, self.stream)
@@ -574,5 +573,15 @@ class B200Backend(Backend):
             self.stream = None
 
 
-def _is_pinned_view(arr: np.ndarray) -> bool:
-    return False
+def _memo_key(args) -> tuple:
+    """Launch-memo key: floats by their bit pattern and type, so 0.0 / -0.0
+    (equal under ==) or 1 / 1.0 never share a bound program."""
+    out = []
+    for a in args:
+        if isinstance(a, (float, np.floating)):
+            out.append((type(a), struct.pack("<d", float(a))))
+        elif isinstance(a, (int, np.integer)) and not isinstance(a, bool):
+            out.append((int, int(a)))
+        else:
+            out.append(a)
+    return tuple(out)

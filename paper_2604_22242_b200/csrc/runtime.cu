@@ -53,24 +53,100 @@ struct ScratchEntry {
 static std::mutex g_scratch_mu;
 static std::map<std::pair<int, void *>, ScratchEntry> g_scratch;
 
+// A zero-filled device block allocated OUTSIDE any stream capture: plain
+// cudaMalloc under a relaxed capture mode (so it is legal while this thread
+// is capturing) and a memset on a private side stream that is synchronised
+// before returning.  Used for memory whose address a CUDA graph may bake in
+// (the scratch arena, allocations made while capturing): a graph memory node
+// would be unmapped between replays and could not be relaunched unfreed.
+static int alloc_outside_capture(void **ptr, size_t bytes) {
+  static thread_local cudaStream_t side[64] = {nullptr};
+  int dev = 0;
+  FM_CHECK(cudaGetDevice(&dev));
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  FM_CHECK(cudaThreadExchangeStreamCaptureMode(&mode));
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e == cudaSuccess && dev < 64 && side[dev] == nullptr)
+    e = cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemsetAsync(*ptr, 0, bytes, side[dev < 64 ? dev : 0]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(side[dev < 64 ? dev : 0]);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (e != cudaSuccess) return fail("alloc_outside_capture", e);
+  return 0;
+}
+
 int get_scratch(void *stream, size_t payload_bytes, Scratch *out) {
   int dev = 0;
   FM_CHECK(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_scratch_mu);
   ScratchEntry &e = g_scratch[{dev, stream}];
-  cudaStream_t s = (cudaStream_t)stream;
   if (e.base == nullptr || e.payload < payload_bytes) {
     // grow geometrically; the outgrown block is retired, not freed, because a
-    // CUDA graph captured earlier (fm_graph_*) may still hold its address
+    // CUDA graph captured earlier (fm_graph_*) may still hold its address.
+    // Never a stream-ordered / graph allocation: the arena's address outlives
+    // any capture that first needed it (eager launches and replays share it).
     size_t want = payload_bytes < (size_t)(1 << 20) ? (size_t)(1 << 20) : payload_bytes;
     if (want < 2 * e.payload) want = 2 * e.payload;
-    FM_CHECK(cudaMallocAsync(&e.base, kCounterBytes + want, s));
-    FM_CHECK(cudaMemsetAsync(e.base, 0, kCounterBytes, s));
+    void *base = nullptr;
+    int st = alloc_outside_capture(&base, kCounterBytes + want);
+    if (st) return st;
+    e.base = base;
     e.payload = want;
   }
   out->counters = (unsigned *)e.base;
   out->payload = (char *)e.base + kCounterBytes;
   out->payload_bytes = e.payload;
+  return 0;
+}
+
+// ---- graph-owned allocations ---------------------------------------------
+// While a thread captures a stream (fm_graph_begin .. fm_graph_end), buffers
+// it allocates are plain (non-graph) allocations and buffers it frees are not
+// released: the graph's kernels reference both on every replay.  They stay
+// alive until the last graph that captured them is destroyed AND the owner
+// has freed them (a temp the planner freed at the end of a captured assign,
+// or an output buffer swapped out by an aliasing assign).  A capture-time
+// allocation that the caller keeps (e.g. the temp an aliasing assign swaps
+// into the output) returns to normal ownership when the graph goes away.
+struct Owned {
+  int graphs = 0;            // live graphs (or the open capture) referencing it
+  bool released = false;     // the owner called fm_free
+  bool plain = false;        // cudaMalloc'ed (else stream-ordered pool memory)
+};
+static std::mutex g_owned_mu;
+static std::map<void *, Owned> g_owned;
+struct CaptureState {
+  bool active = false;
+  std::vector<void *> ptrs;
+};
+static thread_local CaptureState g_capture;
+
+static void owned_add_to_capture(void *p, bool released, bool plain) {
+  Owned &o = g_owned[p];
+  if (o.graphs == 0) o.plain = plain;
+  o.graphs += 1;
+  o.released = o.released || released;
+  g_capture.ptrs.push_back(p);
+}
+
+static int owned_release_refs(const std::vector<void *> &ptrs) {
+  std::vector<std::pair<void *, bool>> to_free;
+  {
+    std::lock_guard<std::mutex> lk(g_owned_mu);
+    for (void *p : ptrs) {
+      auto it = g_owned.find(p);
+      if (it == g_owned.end()) continue;
+      if (--it->second.graphs > 0) continue;
+      if (it->second.released) to_free.push_back({p, it->second.plain});
+      g_owned.erase(it);
+    }
+  }
+  if (to_free.empty()) return 0;
+  FM_CHECK(cudaDeviceSynchronize());   // replays still in flight may use them
+  for (auto &f : to_free) {
+    if (f.second) FM_CHECK(cudaFree(f.first));
+    else FM_CHECK(cudaFreeAsync(f.first, (cudaStream_t)0));
+  }
   return 0;
 }
 
@@ -120,6 +196,14 @@ int fm_device_info(int device, int *sm, int *major, int *minor, int64_t *l2, int
 int fm_alloc(void **ptr, size_t bytes, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (bytes == 0) bytes = 1;
+  if (g_capture.active) {
+    // inside fm_graph_begin/end: a plain allocation owned by the graph
+    int st = alloc_outside_capture(ptr, bytes);
+    if (st) return st;
+    std::lock_guard<std::mutex> lk(g_owned_mu);
+    owned_add_to_capture(*ptr, false, true);
+    return 0;
+  }
   FM_CHECK(cudaMallocAsync(ptr, bytes, s));
   FM_CHECK(cudaMemsetAsync(*ptr, 0, bytes, s));
   return 0;
@@ -127,8 +211,25 @@ int fm_alloc(void **ptr, size_t bytes, void *stream) {
 
 int fm_free(void *ptr, void *stream) {
   if (!ptr) return 0;
+  {
+    std::lock_guard<std::mutex> lk(g_owned_mu);
+    auto it = g_owned.find(ptr);
+    if (it != g_owned.end()) {         // a live graph references it: defer
+      it->second.released = true;
+      return 0;
+    }
+    if (g_capture.active) {            // freed while capturing: the graph keeps it
+      owned_add_to_capture(ptr, true, false);
+      return 0;
+    }
+  }
   FM_CHECK(cudaFreeAsync(ptr, (cudaStream_t)stream));
   return 0;
+}
+
+int64_t fm_graph_owned_count(void) {
+  std::lock_guard<std::mutex> lk(g_owned_mu);
+  return (int64_t)g_owned.size();
 }
 
 int fm_host_alloc(void **ptr, size_t bytes) {
@@ -224,16 +325,27 @@ int fm_event_elapsed_ms(void *start, void *stop, float *ms) {
 struct FmGraph {
   cudaGraphExec_t exec;
   int64_t kernels;
+  std::vector<void *> owned;   // allocations the captured launches reference
 };
 
 int fm_graph_begin(void *stream) {
+  if (g_capture.active) return fail_msg("graph_begin: this thread is already capturing");
   FM_CHECK(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
+  g_capture.active = true;
+  g_capture.ptrs.clear();
   return 0;
 }
 
 int fm_graph_end(void *stream, void **graph, int64_t *kernels) {
   cudaGraph_t g;
-  FM_CHECK(cudaStreamEndCapture((cudaStream_t)stream, &g));
+  g_capture.active = false;
+  std::vector<void *> owned;
+  owned.swap(g_capture.ptrs);
+  cudaError_t ce = cudaStreamEndCapture((cudaStream_t)stream, &g);
+  if (ce != cudaSuccess) {
+    owned_release_refs(owned);
+    return fail("cudaStreamEndCapture", ce);
+  }
   size_t n = 0;
   cudaGraphGetNodes(g, nullptr, &n);
   std::vector<cudaGraphNode_t> nodes(n);
@@ -246,8 +358,11 @@ int fm_graph_end(void *stream, void **graph, int64_t *kernels) {
   cudaGraphExec_t exec;
   cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
   cudaGraphDestroy(g);
-  if (e != cudaSuccess) return fail("cudaGraphInstantiate", e);
-  FmGraph *fg = new FmGraph{exec, k};
+  if (e != cudaSuccess) {
+    owned_release_refs(owned);
+    return fail("cudaGraphInstantiate", e);
+  }
+  FmGraph *fg = new FmGraph{exec, k, std::move(owned)};
   *graph = fg;
   if (kernels) *kernels = k;
   return 0;
@@ -265,9 +380,10 @@ int fm_graph_destroy(void *graph) {
   if (!graph) return 0;
   FmGraph *fg = (FmGraph *)graph;
   cudaError_t e = cudaGraphExecDestroy(fg->exec);
+  std::vector<void *> owned = std::move(fg->owned);
   delete fg;
   if (e != cudaSuccess) return fail("cudaGraphExecDestroy", e);
-  return 0;
+  return owned_release_refs(owned);
 }
 
 }  // extern "C"

@@ -21,11 +21,12 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-from .errors import PlanError
+from . import lower as lw
+from .errors import GenerationError, PlanError
 from .exprtree import (
-    AliasKind, BinaryElem, BinaryKind, Diag, ElemType, ExprNode, InputSpec, Leaf, MatMul,
-    MatShape, Reduce, ReduceKind, ScalarSlot, Subview, Transpose, UnaryElem,
-    UnaryKind, aliases, collect_inputs, signature_of,
+    SCALAR_KINDS, AliasKind, BinaryElem, BinaryKind, Diag, ElemType, ExprNode, InputSpec, Leaf,
+    MatMul, MatShape, Reduce, ReduceKind, ScalarSlot, Subview, Transpose, UnaryElem,
+    UnaryKind, aliases, collect_inputs, signature_of, walk,
 )
 
 COPY = "copy"
@@ -187,7 +188,7 @@ class _Planner:
         return t
 
     def materialize(self, node: ExprNode) -> Leaf:
-        node = self.split(node)
+        node = self.fused(node)
         if isinstance(node, Leaf):
             return node
         t = self.temp(node.shape, node.etype)
@@ -219,13 +220,51 @@ class _Planner:
         self.steps.append(step)
         return step
 
+    def fused(self, node: ExprNode) -> ExprNode:
+        """The MatMul/Reduce-free root of one fused launch: barriers split out
+        (`split`) and the rest cut to the AOT kernels' program limits (`fit`)."""
+        return self.fit(self.split(node))
+
+    # -- program limits -------------------------------------------------------------
+    # One fused launch executes one fm_program: at most MAX_SLOTS leaf
+    # accesses, MAX_INSTR instructions, MAX_SCALARS scalars, MAX_DEPTH stack
+    # registers (include/fmb200.h).  The reference compiles any tree into one
+    # C function (codegen.py:338-391); here a tree past the limits is cut
+    # bottom-up: whenever a node no longer lowers, its largest non-leaf child
+    # (which does, by induction) is materialised into a temp of its own
+    # element type -- bit-identical, since every node already rounds to its
+    # type -- and read back as a dense leaf.
+
+    def fit(self, node: ExprNode) -> ExprNode:
+        if _fits(node):
+            return node
+        return self._fit(node)
+
+    def _fit(self, node: ExprNode) -> ExprNode:
+        if isinstance(node, (Leaf, Subview, Diag)):
+            return node
+        kids = [self._fit(c) for c in node.children()]
+        cur = _rebuild(node, kids)
+        while not _fits(cur):
+            cands = [i for i, c in enumerate(kids) if not isinstance(c, (Leaf, Subview, Diag))]
+            if not cands:
+                # only leaves left and still too big: cannot happen within the
+                # limits (a binary node reads <= 2 leaves), kept as a guard
+                raise PlanError(f"cannot split {type(node).__name__} below the fused-program limits")
+            i = max(cands, key=lambda j: _size(kids[j]))
+            t = self.temp(kids[i].shape, kids[i].etype)
+            self.steps.append(FusedKernelStep.create(kids[i], COPY, t.temp_id))
+            kids[i] = Leaf(t.temp_id, kids[i].etype, kids[i].shape)
+            cur = _rebuild(node, kids)
+        return cur
+
     def split(self, node: ExprNode) -> ExprNode:
         """Replace every MatMul / Reduce subtree with a dense temp leaf."""
         if isinstance(node, MatMul):
             step = self.gemm(node)
             return Leaf(step.out_id, node.etype, node.shape)
         if isinstance(node, Reduce):
-            child = self.split(node.child)
+            child = self.fused(node.child)
             t = self.temp(node.shape, node.etype)
             self.steps.append(FusedKernelStep.create_reduce(
                 child, node.dim, [ReduceOutput(node.kind, t.temp_id, node.etype)]))
@@ -247,6 +286,43 @@ class _Planner:
             c = self.split(node.child)
             return node if c is node.child else Transpose(c)
         raise PlanError(f"cannot plan node {type(node).__name__}")
+
+
+def _size(node: ExprNode) -> int:
+    return sum(1 for _ in walk(node))
+
+
+def _fits(node: ExprNode) -> bool:
+    """Does `node` lower within the fused-program limits?  Cheap bound first
+    (every node emits at most two instructions), the real lowering otherwise."""
+    n = leaves = scalars = 0
+    for x in walk(node):
+        n += 1
+        if isinstance(x, (Leaf, Subview, Diag)):
+            leaves += 1
+        elif isinstance(x, UnaryElem) and x.kind in SCALAR_KINDS:
+            scalars += 1
+    if 2 * n <= lw.MAX_INSTR and leaves <= lw.MAX_SLOTS and scalars <= lw.MAX_SCALARS:
+        return True
+    try:
+        lw.lower(node)
+        return True
+    except GenerationError:
+        return False
+
+
+def _rebuild(node: ExprNode, kids: list) -> ExprNode:
+    old = node.children()
+    if all(a is b for a, b in zip(old, kids)):
+        return node
+    if isinstance(node, UnaryElem):
+        return UnaryElem(node.kind, kids[0], scalar=node.scalar, exponent=node.exponent,
+                         target=node.target)
+    if isinstance(node, BinaryElem):
+        return BinaryElem(node.kind, kids[0], kids[1])
+    if isinstance(node, Transpose):
+        return Transpose(kids[0])
+    raise PlanError(f"cannot rebuild node {type(node).__name__}")
 
 
 def _scaled(node: ExprNode) -> tuple[ExprNode, float]:
@@ -317,14 +393,14 @@ def plan(out_mat_id: int, node: ExprNode) -> ExecutionPlan:
                              out_is_temp=unsafe)
 
     if isinstance(node, Reduce):
-        child = p.split(node.child)
+        child = p.fused(node.child)
         target = p.temp(node.shape, node.etype).temp_id if unsafe else out_mat_id
         p.steps.append(FusedKernelStep.create_reduce(
             child, node.dim, [ReduceOutput(node.kind, target, node.etype)]))
         return ExecutionPlan(p.steps, p.temps, target, node.shape, node.etype,
                              out_is_temp=unsafe)
 
-    root = p.split(node)
+    root = p.fused(node)
     if unsafe:
         t = p.temp(root.shape, root.etype)
         p.steps.append(FusedKernelStep.create(root, COPY, t.temp_id))
@@ -337,7 +413,7 @@ def plan(out_mat_id: int, node: ExprNode) -> ExecutionPlan:
 def reduce_plan(node: ExprNode, finalize: int = FINAL_NONE) -> ExecutionPlan:
     """Full reduction into a 1x1 accumulator temp (`plan.py:208-215`)."""
     p = _Planner()
-    root = p.split(node)
+    root = p.fused(node)
     acc = p.temp(MatShape(1, 1), accumulator_type(root.etype))
     p.steps.append(FusedKernelStep.create(root, REDUCE_ACCU, acc.temp_id, finalize))
     return ExecutionPlan(p.steps, p.temps, acc.temp_id, acc.shape, acc.etype,
@@ -351,20 +427,31 @@ def _binding_key(node: ExprNode):
     return (signature_of(node),
             tuple((s.mat_id, tuple((v.kind, v.row_off, v.col_off) for v in s.views))
                   for s in inputs),
-            tuple(s.value for s in scalars))
+            tuple((type(s.value), repr(s.value)) for s in scalars))
 
 
 def plan_many(assignments: list[tuple[int, ExprNode]]) -> ExecutionPlan:
     """Plan several assignments together.  Reduce roots along the same dim of
     the same bound subexpression fuse into one multi-output launch (C4's
     sum/mean/max/index_max read X, Y, Z once); everything else plans as
-    `plan` would, in order.  Outputs must not alias any input."""
+    `plan` would, in order.  No output may be an input of ANY assignment in
+    the batch (a grouped reduction is hoisted to its group's first position,
+    so a write between two members would otherwise change what the later
+    ones read), and no matrix may be written twice."""
     p = _Planner()
     groups: dict = {}
     order: list = []
+    outs_seen: set = set()
+    read: set = set()
     for out_id, node in assignments:
-        if aliases(out_id, node) is not AliasKind.NONE:
-            raise PlanError("plan_many outputs may not alias their inputs")
+        if out_id in outs_seen:
+            raise PlanError(f"plan_many writes matrix {out_id} twice")
+        outs_seen.add(out_id)
+        read.update(spec.mat_id for spec in collect_inputs(node)[0])
+    clash = outs_seen & read
+    if clash:
+        raise PlanError(f"plan_many outputs may not be read by the batch (matrices {sorted(clash)})")
+    for out_id, node in assignments:
         if isinstance(node, Reduce):
             key = (node.dim, _binding_key(node.child))
             if key not in groups:
@@ -376,14 +463,14 @@ def plan_many(assignments: list[tuple[int, ExprNode]]) -> ExecutionPlan:
     for item in order:
         if item in groups:
             node, outs = groups[item]
-            child = p.split(node.child)
+            child = p.fused(node.child)
             p.steps.append(FusedKernelStep.create_reduce(child, node.dim, outs))
         else:
             out_id, node = item
             if isinstance(node, MatMul):
                 p.gemm(node, out_id)
             else:
-                root = p.split(node)
+                root = p.fused(node)
                 p.steps.append(FusedKernelStep.create(root, COPY, out_id))
     last = assignments[-1]
     return ExecutionPlan(p.steps, p.temps, last[0], last[1].shape, last[1].etype)

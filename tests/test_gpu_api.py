@@ -385,6 +385,76 @@ def test_graph_capture_replays_the_same_kernels(ctx):
     g.close()
 
 
+def test_capture_on_a_fresh_backend_replays_twice():
+    """A reduction whose scratch arena is first needed INSIDE a capture (fresh
+    backend = fresh stream): the arena is a plain allocation, not a graph
+    memory node, so the graph relaunches and eager launches share it."""
+    from paper_2604_22242_b200._native import native
+    ctx = fm.Context(fm.B200Backend())
+    n = 1 << 18
+    x = fm.randu(n, 1, 21, "f64", ctx)
+    y = fm.randu(n, 1, 22, "f64", ctx)
+    r = fm.Mat(1, 1, "f64", ctx)
+    g = fm.capture(lambda: fm.dot_async(x, y, r, 0), ctx)
+    want = orc.accu(x.to_numpy() * y.to_numpy(), orc.ElemType.f64)
+    for _ in range(2):
+        r.set_values(np.zeros((1, 1)))
+        g.replay()
+        assert abs(r.to_numpy()[0, 0] - want) <= 1e-12 * abs(want)
+    assert abs(fm.dot(x, y) - want) <= 1e-12 * abs(want)     # eager after capture
+    g.close()
+    ctx.backend.close()
+    assert native().lib.fm_graph_owned_count() == 0
+
+
+def test_capture_of_an_aliasing_assign_owns_its_buffers(ctx):
+    """Z.assign(Z.t() + X) plans through a temp that is swapped into Z.  Under
+    capture the temp and Z's old buffer belong to the graph until it is
+    destroyed; the graph replays (twice) and nothing is freed under it."""
+    from paper_2604_22242_b200._native import native
+    base = native().lib.fm_graph_owned_count()
+    n = 64
+    Z = fm.randu(n, n, 31, "f32", ctx)
+    X = fm.randu(n, n, 32, "f32", ctx)
+    z0, xv = Z.to_numpy().copy(), X.to_numpy()
+    g = fm.capture(lambda: Z.assign(Z.t() + X), ctx)
+    assert native().lib.fm_graph_owned_count() == base + 2
+    for _ in range(2):
+        g.replay()
+        assert np.array_equal(Z.to_numpy(), z0.T + xv)   # reads the captured (old) buffer
+    g.close()
+    assert native().lib.fm_graph_owned_count() == base   # old buffer freed, temp returned to Z
+    Z.assign(Z + X)                                     # Z's buffer is still valid
+    assert np.array_equal(Z.to_numpy(), (z0.T + xv) + xv)
+
+
+@pytest.mark.parametrize("n_terms", [48, 64])
+def test_addn_past_the_program_limits(ctx, n_terms):
+    """add-N beyond one fused program (40 leaf reads): the planner splits it
+    into ceil((N-1)/39) launches through temps, still bit-exact."""
+    mats = [fm.randu(129, 65, seed=100 + i, ctx=ctx) for i in range(n_terms)]
+    e = mats[0] + mats[1]
+    for m in mats[2:]:
+        e = e + m
+    z = fm.zeros(129, 65, ctx=ctx)
+    ctx.reset_counters()
+    z.assign(e)
+    assert ctx.launches == -(-(n_terms - 1) // 39)
+    want = mats[0].to_numpy() + mats[1].to_numpy()
+    for m in mats[2:]:
+        want = want + m.to_numpy()
+    assert np.array_equal(z.to_numpy(), want)
+
+
+def test_signed_zero_scalars_do_not_share_a_bound_program(ctx):
+    x = fm.randu(16, 16, 5, "f32", ctx)
+    z = fm.zeros(16, 16, ctx=ctx)
+    z.assign(x * 0.0)
+    assert not np.signbit(z.to_numpy()).any()
+    z.assign(x * -0.0)
+    assert np.signbit(z.to_numpy()).all()
+
+
 def test_log_f32_sweep_vs_correctly_rounded(ctx):
     """log_f (ops.cuh, table-driven) over a dense sweep of positive f32 bit
     patterns (subnormals to FLT_MAX), every f32 within 2^-6 of 1, and the

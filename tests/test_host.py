@@ -160,6 +160,56 @@ def test_lowering_limits():
         lower.lower(big)
 
 
+def _addn(n, t=F32):
+    e = L(0, t=t)
+    for i in range(1, n):
+        e = ast.plus(e, L(i, t=t))
+    return e
+
+
+@pytest.mark.parametrize("n", [40, 41, 48, 64, 200])
+def test_planner_splits_trees_past_the_program_limits(n):
+    """add-N for any N (reference bench.py:307-326 sweeps it unbounded): the
+    planner cuts the tree into launches that each lower within the limits,
+    materialising sub-sums into temps; every input is read exactly once."""
+    pl = P.plan(OUT, _addn(n))
+    steps = pl.fused_steps
+    assert len(steps) == -(-(n - 1) // (lower.MAX_SLOTS - 1)) if n > lower.MAX_SLOTS else len(steps) == 1
+    reads = []
+    for st in steps:
+        prog = lower.lower(st.expr)                      # each launch lowers
+        assert len(prog.slots) <= lower.MAX_SLOTS
+        reads += [s.mat_id for s in st.inputs if s.mat_id >= 0]
+    assert sorted(reads) == list(range(n))
+    assert steps[-1].out_id == OUT
+    temps = {t.temp_id for t in pl.temps}
+    for st in steps[:-1]:
+        assert st.out_id in temps
+
+
+def test_planner_splits_on_scalar_count():
+    e = L(0)
+    for i in range(40):
+        e = ast.scalar_add(e, float(i))           # 40 scalars > MAX_SCALARS
+    pl = P.plan(OUT, e)
+    assert len(pl.fused_steps) == 2
+    for st in pl.fused_steps:
+        assert len(lower.lower(st.expr).scalars) <= lower.MAX_SCALARS
+
+
+def test_plan_many_rejects_outputs_read_by_the_batch():
+    from paper_2604_22242_b200.errors import PlanError
+    X, Y = L(0), L(1)
+    red = lambda k, n: ast.reduce(k, 0, n)  # noqa: E731
+    with pytest.raises(PlanError):
+        P.plan_many([(10, red(ast.ReduceKind.sum, X)), (0, ast.scalar_add(Y, 1.0)),
+                      (11, red(ast.ReduceKind.max, X))])
+    with pytest.raises(PlanError):
+        P.plan_many([(10, red(ast.ReduceKind.sum, X)), (10, red(ast.ReduceKind.max, X))])
+    pl = P.plan_many([(10, red(ast.ReduceKind.sum, X)), (11, red(ast.ReduceKind.max, X))])
+    assert len(pl.steps) == 1
+
+
 def test_bf16_nodes_round_after_every_op():
     x = L(0, t=ElemType.bf16)
     p = lower.lower(ast.plus(ast.scalar_pre_mul(2.5, x), x))
