@@ -229,6 +229,44 @@ int fm_graph_destroy(void *graph);
  * Returns how many such buffers are currently alive (tests). */
 int64_t fm_graph_owned_count(void);
 
+/* ---- collectives of the column-sharded path (csrc/comm.cu) -----------------
+ * New API: the reference has no multi-device code.  A
+ * communicator joins one rank per process (per GPU).  Every collective
+ * gathers the ranks' contributions and combines them IN RANK ORDER, so all
+ * ranks get bit-identical results whatever the transport:
+ *   FM_COMM_PEER -- one kernel per collective over CUDA-IPC peer memory
+ *                   (NVLink between GPUs; also works for ranks sharing a GPU)
+ *   FM_COMM_NCCL -- ncclAllGather (libnccl dlopen'ed) + a combine kernel
+ * All calls are stream-ordered and may be captured into CUDA graphs.       */
+enum { FM_COMM_NCCL = 1, FM_COMM_PEER = 2 };
+enum { FM_COMBINE_SUM = 0, FM_COMBINE_MAX = 1, FM_COMBINE_MIN = 2 };
+
+int fm_comm_nccl_load(const char *path);            /* NULL: "libnccl.so.2" */
+int fm_comm_nccl_version(int *version);
+int fm_comm_nccl_unique_id(uint8_t *id128);         /* rank 0 makes it, the others receive it */
+int fm_comm_init_nccl(void **comm, int nranks, int rank, const uint8_t *id128);
+/* peer transport: each rank allocates its exchange block (header + 2 data
+ * parities of `slot_bytes`) and shares the 64-byte IPC handle; then every
+ * rank opens the others' blocks with all nranks handles (rank order) */
+int fm_comm_peer_block(void **block, size_t slot_bytes, uint8_t *ipc_handle64);
+int fm_comm_init_peer(void **comm, int nranks, int rank, void *block, const uint8_t *handles,
+                      size_t slot_bytes);
+int fm_comm_destroy(void *comm);
+int fm_comm_info(void *comm, int *nranks, int *rank, int *transport);
+int fm_comm_status(void *comm, int64_t *error);      /* peer: nonzero if a wait timed out (30 s) */
+/* in place: buf = combine over ranks (rank order) of every rank's buf;
+ * FM_F32 / FM_F64 / FM_U32 / FM_I32; SUM (ints wrap), MAX / MIN (NaN
+ * propagates); divisor > 0 divides the combined value (mean of f64 sums) */
+int fm_allreduce(void *comm, void *buf, int64_t count, int32_t etype, int32_t op, double divisor,
+                 void *stream);
+/* in place arg-select: per element the (value, index) pair of the extreme
+ * over ranks -- first index wins ties, NaN wins (numpy argmax / argmin);
+ * `idx_offset` is added to this rank's indices first (local -> global) */
+int fm_allreduce_arg(void *comm, void *vals, uint32_t *idx, int64_t count, int32_t etype,
+                     uint32_t idx_offset, int32_t maximize, void *stream);
+/* dst[q * bytes .. (q+1) * bytes) = rank q's src, on every rank */
+int fm_allgather(void *comm, const void *src, size_t bytes, void *dst, void *stream);
+
 /* number of kernels this library launched since load (for bench gpu_launches) */
 int64_t fm_launch_counter(void);
 

@@ -122,6 +122,19 @@ SIGNATURES = {
     "fm_graph_launch": [_P, _P],
     "fm_graph_destroy": [_P],
     "fm_graph_owned_count": [],
+    "fm_comm_nccl_load": [ctypes.c_char_p],
+    "fm_comm_nccl_version": [ctypes.POINTER(ctypes.c_int)],
+    "fm_comm_nccl_unique_id": [ctypes.c_char_p],
+    "fm_comm_init_nccl": [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int, ctypes.c_char_p],
+    "fm_comm_peer_block": [ctypes.POINTER(_P), _SZ, ctypes.c_char_p],
+    "fm_comm_init_peer": [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int, _P, ctypes.c_char_p, _SZ],
+    "fm_comm_destroy": [_P],
+    "fm_comm_info": [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                     ctypes.POINTER(ctypes.c_int)],
+    "fm_comm_status": [_P, ctypes.POINTER(_I64)],
+    "fm_allreduce": [_P, _P, _I64, _I32, _I32, ctypes.c_double, _P],
+    "fm_allreduce_arg": [_P, _P, _P, _I64, _I32, ctypes.c_uint32, _I32, _P],
+    "fm_allgather": [_P, _P, _SZ, _P, _P],
     "fm_launch_counter": [],
 }
 _RESTYPES = {"fm_last_error": ctypes.c_char_p, "fm_launch_counter": ctypes.c_int64,

@@ -26,7 +26,7 @@ LIB = PKG / "libfmb200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-v", "-I", str(INCLUDE), "-I", str(CSRC)]
-SOURCES = ["runtime.cu", "fused.cu", "rng.cu", "gemm_simt.cu", "gemm_tc.cu"]
+SOURCES = ["runtime.cu", "fused.cu", "rng.cu", "gemm_simt.cu", "gemm_tc.cu", "comm.cu"]
 
 
 def units() -> list[tuple[str, str, list[str]]]:
@@ -92,7 +92,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             stale.unlink()
     if force or jobs or not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
         tmp = LIB.with_suffix(".so.tmp")
-        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

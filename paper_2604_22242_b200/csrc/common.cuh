@@ -25,6 +25,9 @@ struct Scratch {
   size_t payload_bytes;
 };
 int get_scratch(void *stream, size_t payload_bytes, Scratch *out);
+// zero-filled plain cudaMalloc made outside any stream capture (safe to call
+// while this thread captures; the address can be baked into a graph)
+int alloc_plain(void **ptr, size_t bytes);
 
 int sm_count();
 

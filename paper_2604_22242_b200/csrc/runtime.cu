@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 
 #include <vector>
@@ -59,7 +60,7 @@ static std::map<std::pair<int, void *>, ScratchEntry> g_scratch;
 // before returning.  Used for memory whose address a CUDA graph may bake in
 // (the scratch arena, allocations made while capturing): a graph memory node
 // would be unmapped between replays and could not be relaunched unfreed.
-static int alloc_outside_capture(void **ptr, size_t bytes) {
+int alloc_plain(void **ptr, size_t bytes) {
   static thread_local cudaStream_t side[64] = {nullptr};
   int dev = 0;
   FM_CHECK(cudaGetDevice(&dev));
@@ -71,7 +72,7 @@ static int alloc_outside_capture(void **ptr, size_t bytes) {
   if (e == cudaSuccess) e = cudaMemsetAsync(*ptr, 0, bytes, side[dev < 64 ? dev : 0]);
   if (e == cudaSuccess) e = cudaStreamSynchronize(side[dev < 64 ? dev : 0]);
   cudaThreadExchangeStreamCaptureMode(&mode);
-  if (e != cudaSuccess) return fail("alloc_outside_capture", e);
+  if (e != cudaSuccess) return fail("alloc_plain", e);
   return 0;
 }
 
@@ -88,7 +89,7 @@ int get_scratch(void *stream, size_t payload_bytes, Scratch *out) {
     size_t want = payload_bytes < (size_t)(1 << 20) ? (size_t)(1 << 20) : payload_bytes;
     if (want < 2 * e.payload) want = 2 * e.payload;
     void *base = nullptr;
-    int st = alloc_outside_capture(&base, kCounterBytes + want);
+    int st = alloc_plain(&base, kCounterBytes + want);
     if (st) return st;
     e.base = base;
     e.payload = want;
@@ -115,6 +116,9 @@ struct Owned {
 };
 static std::mutex g_owned_mu;
 static std::map<void *, Owned> g_owned;
+// plain (cudaMalloc) buffers that went back to their owner after the graphs
+// that captured them were destroyed: freed with cudaFree, not cudaFreeAsync
+static std::set<void *> g_plain;
 struct CaptureState {
   bool active = false;
   std::vector<void *> ptrs;
@@ -138,6 +142,7 @@ static int owned_release_refs(const std::vector<void *> &ptrs) {
       if (it == g_owned.end()) continue;
       if (--it->second.graphs > 0) continue;
       if (it->second.released) to_free.push_back({p, it->second.plain});
+      else if (it->second.plain) g_plain.insert(p);
       g_owned.erase(it);
     }
   }
@@ -198,7 +203,7 @@ int fm_alloc(void **ptr, size_t bytes, void *stream) {
   if (bytes == 0) bytes = 1;
   if (g_capture.active) {
     // inside fm_graph_begin/end: a plain allocation owned by the graph
-    int st = alloc_outside_capture(ptr, bytes);
+    int st = alloc_plain(ptr, bytes);
     if (st) return st;
     std::lock_guard<std::mutex> lk(g_owned_mu);
     owned_add_to_capture(*ptr, false, true);
@@ -215,11 +220,20 @@ int fm_free(void *ptr, void *stream) {
     std::lock_guard<std::mutex> lk(g_owned_mu);
     auto it = g_owned.find(ptr);
     if (it != g_owned.end()) {         // a live graph references it: defer
-      it->second.released = true;
+      if (g_capture.active) owned_add_to_capture(ptr, true, it->second.plain);
+      else it->second.released = true;
       return 0;
     }
+    bool plain = g_plain.count(ptr) > 0;
     if (g_capture.active) {            // freed while capturing: the graph keeps it
-      owned_add_to_capture(ptr, true, false);
+      if (plain) g_plain.erase(ptr);
+      owned_add_to_capture(ptr, true, plain);
+      return 0;
+    }
+    if (plain) {
+      g_plain.erase(ptr);
+      FM_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+      FM_CHECK(cudaFree(ptr));
       return 0;
     }
   }

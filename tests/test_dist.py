@@ -1,11 +1,15 @@
-"""World-size-2 gloo tests of the column-sharded combine logic.
+"""The column-sharded public API over gloo on CPU, world sizes 2 and 3.
 
-The N>1 path is: every rank owns a contiguous column block (a contiguous
-slice of the column-major element stream, so randu of a shard equals that
-slice of the global randu stream); elementwise work is local; only reduction
-partials cross ranks.  These tests run that host logic over gloo on CPU with
-the oracle supplying each rank's local partials, and check the combined
-result against the single-process oracle on the whole matrix.
+SURVEY.md 8(e).  Every rank builds `ShardedMat`s of one global matrix (its
+column block = its slice of the global splitmix64 stream) on a host
+simulation of the device (tests/hostsim.py: oracle-evaluated launches) and
+calls the same public functions a GPU user calls -- `fm.sum/mean/max/min/
+index_max/index_min(e, dim)`, `fm.assign_all`, `fm.accu/dot/norm`,
+`ShardedMat.assign`, `fm.matmul_row_shard` -- with the collectives of
+csrc/comm.cu restated over gloo (tests/hostsim.SimComm).  Results must equal
+the single-process oracle on the whole matrix: bit-exact for elementwise
+chains, indices and extrema, within 1e-12 for sums.  The native collectives
+themselves run on the GPU (tests/test_gpu_dist.py).
 """
 
 import os
@@ -13,13 +17,11 @@ import socket
 
 import numpy as np
 import pytest
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import fm_oracle as orc
-from paper_2604_22242_b200.dist import (allreduce_rowstats, allreduce_sum, column_shard,
-                                        combine_arg_candidates, combine_norm)
+from paper_2604_22242_b200.dist import column_shard, row_block
 from paper_2604_22242_b200.errors import ShapeError
 
 
@@ -45,81 +47,105 @@ def _entry(rank, world, port, fn, args):
         dist.destroy_process_group()
 
 
+def _setup(rank, world):
+    import paper_2604_22242_b200 as fm
+    from hostsim import SimBackend, SimComm
+    ctx = fm.Context(SimBackend())
+    return fm, ctx, SimComm(ctx, rank, world)
+
+
 # ---- rank bodies (module-level so spawn can pickle them) -----------------------------
 
-def _body_full_reductions(rank, world, n_rows, n_cols):
-    sh = column_shard(n_rows, n_cols, rank, world)
-    n_loc = sh.n_rows * sh.local_cols
-    for ety in (orc.ElemType.f32, orc.ElemType.f64):
-        x = orc.uniform_fill(42, n_loc, ety.value, offset=sh.elem_offset)
-        y = orc.uniform_fill(43, n_loc, ety.value, offset=sh.elem_offset)
-        part = torch.tensor([orc.accu(x * y, ety), orc.accu((x - y) * (x - y), ety)], dtype=torch.float64)
-        allreduce_sum(part)
-        gx = orc.uniform_fill(42, n_rows * n_cols, ety.value)
-        gy = orc.uniform_fill(43, n_rows * n_cols, ety.value)
+def _body_elementwise_and_full(rank, world, n_rows, n_cols):
+    fm, ctx, comm = _setup(rank, world)
+    for et in ("f32", "f64"):
+        X = fm.ShardedMat(n_rows, n_cols, et, comm).randu(42)
+        Y = fm.ShardedMat(n_rows, n_cols, et, comm).randu(43)
+        Z = fm.ShardedMat(n_rows, n_cols, et, comm)
+        gx, gy = orc.randu(n_rows, n_cols, 42, et), orc.randu(n_rows, n_cols, 43, et)
+        assert np.array_equal(X.to_numpy(), gx)              # shard = slice of the global stream
+        Z.assign(fm.exp(-fm.square(X - Y) / 2) + 0.5 * fm.abs(X))     # C3, no exchange
+        dt = np.float32 if et == "f32" else np.float64
+        half = dt(0.5)
+        d = gx - gy
+        want = np.exp((half * -(d * d)).astype(np.float64)).astype(dt) + half * np.abs(gx)
+        assert orc.max_ulp(Z.to_numpy(), want) == 0
+        ety = orc.ElemType.of(et)
         want_dot = orc.accu(gx * gy, ety)
-        want_norm = float(np.sqrt(orc.accu((gx - gy) * (gx - gy), ety)))
-        assert abs(part[0].item() - want_dot) <= 1e-12 * abs(want_dot)
-        assert abs(combine_norm(part[1].item()) - want_norm) <= 1e-12 * want_norm
+        assert abs(fm.dot(X, Y) - want_dot) <= 1e-12 * abs(want_dot)
+        assert abs(fm.accu(X % Y) - want_dot) <= 1e-12 * abs(want_dot)
+        want_norm = float(np.sqrt(orc.accu(d * d, ety)))
+        assert abs(fm.norm(X - Y) - want_norm) <= 1e-12 * want_norm
+    calls = [c[0] for c in comm.calls]
+    assert "allreduce" in calls
 
 
-def _body_row_stats(rank, world, n_rows, n_cols):
-    sh = column_shard(n_rows, n_cols, rank, world)
-    g = orc.randu(n_rows, n_cols, 7, "f64")
-    g[3, 5] = g[3, 9] = 2.0            # a tie across the shard boundary: first index wins
-    g[7, 0] = np.nan                   # NaN wins index_max (numpy argmax semantics)
-    g[11, 2] = -1.0
-    g[11, 12] = -1.0                   # tie for index_min
-    loc = g[:, sh.col0:sh.col1]
+def _body_dim_reductions(rank, world, n_rows, n_cols):
+    fm, ctx, comm = _setup(rank, world)
     ety = orc.ElemType.f64
-    sums = torch.tensor(orc.reduce_dim(orc.ReduceKind.sum, 1, loc, ety).ravel())
-    maxs = torch.tensor(loc.max(axis=1))
-    mins = torch.tensor(loc.min(axis=1))
-    allreduce_rowstats(sums, maxs, mins)
-    want_sum = orc.reduce_dim(orc.ReduceKind.sum, 1, g, ety).ravel()
-    assert orc.compare(sums.numpy(), want_sum) < 1e-13     # NaN-aware (oracle.py:104-123)
-    assert np.array_equal(mins.numpy(), g.min(axis=1), equal_nan=True)
-    assert np.array_equal(maxs.numpy(), g.max(axis=1), equal_nan=True)
-    for maximize, kind in ((True, orc.ReduceKind.index_max), (False, orc.ReduceKind.index_min)):
-        li = (np.argmax(loc, axis=1) if maximize else np.argmin(loc, axis=1))
-        lv = loc[np.arange(n_rows), li]
-        bv, bi = combine_arg_candidates(torch.tensor(lv), torch.tensor(li + sh.col0, dtype=torch.int64),
-                                        maximize)
-        want = orc.reduce_dim(kind, 1, g, ety).ravel()
-        assert np.array_equal(bi.numpy(), want.astype(np.int64)), (maximize, bi.numpy(), want)
-
-
-def _body_column_local(rank, world, n_rows, n_cols):
-    """dim-0 stats are shard-local: the gathered per-shard results equal the
-    whole-matrix result with no partial combine."""
+    g = [orc.randu(n_rows, n_cols, s, "f64") for s in (42, 43, 44)]
+    g[0][3, 5] = g[0][3, 9] = 9.0      # ties across shard boundaries: first index wins
+    g[1][3, 5] = g[1][3, 9] = 0.0
+    g[2][3, 5] = g[2][3, 9] = 1.0
+    g[0][7, n_cols - 1] = np.nan       # NaN wins index_max / propagates through max
+    X, Y, Z = (fm.ShardedMat(n_rows, n_cols, "f64", comm).set_global(a) for a in g)
+    e = (X - Y) % Z
+    v = (g[0] - g[1]) * g[2]
+    K = orc.ReduceKind
+    # dim 0: column-sharded results, no exchange
+    outs0 = [fm.ShardedMat(1, n_cols, t, comm) for t in ("f64", "f64", "f64", "u32", "f64", "u32")]
+    comm.calls.clear()
+    fm.assign_all([(outs0[0], fm.sum(e, 0)), (outs0[1], fm.mean(e, 0)), (outs0[2], fm.max(e, 0)),
+                   (outs0[3], fm.index_max(e, 0)), (outs0[4], fm.min(e, 0)), (outs0[5], fm.index_min(e, 0))])
+    assert comm.calls == []
+    for o, k in zip(outs0, (K.sum, K.mean, K.max, K.index_max, K.min, K.index_min)):
+        want = orc.reduce_dim(k, 0, v, ety)
+        got = o.to_numpy()
+        if k in (K.sum, K.mean):
+            assert orc.compare(got, want) < 1e-13
+        else:
+            assert np.array_equal(got, want, equal_nan=True), k
+    # dim 1: replicated n_rows x 1 results through the collectives
+    outs1 = [fm.Mat(n_rows, 1, t, ctx) for t in ("f64", "f64", "f64", "u32", "f64", "u32")]
+    fm.assign_all([(outs1[0], fm.sum(e, 1)), (outs1[1], fm.mean(e, 1)), (outs1[2], fm.max(e, 1)),
+                   (outs1[3], fm.index_max(e, 1)), (outs1[4], fm.min(e, 1)), (outs1[5], fm.index_min(e, 1))])
+    for o, k in zip(outs1, (K.sum, K.mean, K.max, K.index_max, K.min, K.index_min)):
+        want = orc.reduce_dim(k, 1, v, ety)
+        got = o.to_numpy()
+        if k in (K.sum, K.mean):
+            assert orc.compare(got, want) < 1e-13
+        else:
+            assert np.array_equal(got, want, equal_nan=True), k
     sh = column_shard(n_rows, n_cols, rank, world)
-    ety = orc.ElemType.f64
-    x = orc.uniform_fill(42, sh.n_rows * sh.local_cols, "f64", offset=sh.elem_offset).reshape(
-        (n_rows, sh.local_cols), order="F")
-    y = orc.uniform_fill(43, sh.n_rows * sh.local_cols, "f64", offset=sh.elem_offset).reshape(
-        (n_rows, sh.local_cols), order="F")
-    v = (x - y) * x
-    loc_sum = torch.tensor(orc.reduce_dim(orc.ReduceKind.sum, 0, v, ety).ravel())
-    loc_idx = torch.tensor(orc.reduce_dim(orc.ReduceKind.index_max, 0, v, ety).ravel().astype(np.int64))
-    counts = [column_shard(n_rows, n_cols, r, world).local_cols for r in range(world)]
-    sums = [torch.empty(c, dtype=torch.float64) for c in counts]
-    idxs = [torch.empty(c, dtype=torch.int64) for c in counts]
-    # gloo all_gather needs equal sizes: pad to the largest block
-    m = max(counts)
-    ps = torch.zeros(m, dtype=torch.float64)
-    ps[:loc_sum.numel()] = loc_sum
-    pi = torch.zeros(m, dtype=torch.int64)
-    pi[:loc_idx.numel()] = loc_idx
-    gs = [torch.empty(m, dtype=torch.float64) for _ in range(world)]
-    gi = [torch.empty(m, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(gs, ps)
-    dist.all_gather(gi, pi)
-    sums = np.concatenate([g[:c].numpy() for g, c in zip(gs, counts)])
-    idxs = np.concatenate([g[:c].numpy() for g, c in zip(gi, counts)])
-    gx, gy = orc.randu(n_rows, n_cols, 42, "f64"), orc.randu(n_rows, n_cols, 43, "f64")
-    gv = (gx - gy) * gx
-    assert orc.compare(sums, orc.reduce_dim(orc.ReduceKind.sum, 0, gv, ety).ravel()) < 1e-14
-    assert np.array_equal(idxs, orc.reduce_dim(orc.ReduceKind.index_max, 0, gv, ety).ravel())
+    assert ("allreduce_arg", True, n_rows, sh.col0) in comm.calls
+    assert ("allreduce", "sum", n_rows, float(n_cols)) in comm.calls     # mean: / global n_cols
+    # a single lazy reduction through eval()
+    s1 = fm.sum(e, 1).eval()
+    assert orc.compare(s1.to_numpy(), orc.reduce_dim(K.sum, 1, v, ety)) < 1e-13
+
+
+def _body_f32_row_sum(rank, world, n_rows, n_cols):
+    """f32 children: partial row sums travel as f64 and round once."""
+    fm, ctx, comm = _setup(rank, world)
+    X = fm.ShardedMat(n_rows, n_cols, "f32", comm).randu(5)
+    gx = orc.randu(n_rows, n_cols, 5, "f32")
+    out = fm.Mat(n_rows, 1, "f32", ctx)
+    fm.assign_all([(out, fm.mean(X * X, 1))])
+    want = orc.reduce_dim(orc.ReduceKind.mean, 1, gx * gx, orc.ElemType.f32)
+    assert np.array_equal(out.to_numpy(), want)
+
+
+def _body_row_shard_gemm(rank, world, m, n, k):
+    fm, ctx, comm = _setup(rank, world)
+    r0, r1 = row_block(m, rank, world)
+    gx = orc.randu(m, k, 42, "f32")
+    X_rows = fm.from_array(np.ascontiguousarray(gx[r0:r1]), "f32", ctx)
+    Y = fm.ShardedMat(n, k, "f32", comm).randu(43)
+    gy = orc.randu(n, k, 43, "f32")
+    Z = fm.matmul_row_shard(X_rows, Y, 2.0)
+    want = (2.0 * (gx[r0:r1].astype(np.float64) @ gy.astype(np.float64).T)).astype(np.float32)
+    assert np.array_equal(Z.to_numpy(), want)
+    assert ("allgather", n * k // world) in comm.calls
 
 
 # ---- tests -------------------------------------------------------------------------------
@@ -148,13 +174,34 @@ def test_shard_stream_is_global_slice():
         assert np.array_equal(loc, g[:, sh.col0:sh.col1])
 
 
-def test_gloo_full_reductions_world2():
-    _run(2, _body_full_reductions, 1000, 37)
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_elementwise_and_full_reductions(world):
+    _run(world, _body_elementwise_and_full, 40, 17)
 
 
-def test_gloo_row_stats_world2():
-    _run(2, _body_row_stats, 16, 14)
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_dim_reductions(world):
+    _run(world, _body_dim_reductions, 24, 14)
 
 
-def test_gloo_column_stats_local_world2():
-    _run(2, _body_column_local, 128, 9)
+def test_sharded_f32_row_mean_world2():
+    _run(2, _body_f32_row_sum, 32, 9)
+
+
+def test_row_sharded_gemm_world2():
+    _run(2, _body_row_shard_gemm, 16, 12, 8)
+
+
+def test_sharded_api_rejects_locality_breaking_ops():
+    import paper_2604_22242_b200 as fm
+    from hostsim import SimBackend, SimComm
+    ctx = fm.Context(SimBackend())
+    comm = SimComm(ctx, 0, 1)
+    X = fm.ShardedMat(4, 4, "f32", comm)
+    M = fm.Mat(4, 4, "f32", ctx)
+    with pytest.raises(ShapeError):
+        X.t()
+    with pytest.raises(ShapeError):
+        X + M
+    with pytest.raises(ShapeError):
+        X + fm.ShardedMat(4, 5, "f32", comm)
