@@ -161,6 +161,9 @@ int fm_set_device(int device);
 int fm_get_device(int *device);
 int fm_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,
                    int64_t *l2_bytes, int64_t *hbm_bytes);
+/* "0000:1b:00.0"-style id: identifies a GPU across processes whatever their
+ * CUDA_VISIBLE_DEVICES numbering (transport choice of the sharded path) */
+int fm_device_pci_bus_id(int device, char *buf, int len);
 
 /* ---- memory (backend.py:192-239) ---------------------------------------- */
 int fm_alloc(void **ptr, size_t bytes, void *stream);          /* zero-filled */

@@ -88,6 +88,7 @@ SIGNATURES = {
     "fm_get_device": [ctypes.POINTER(ctypes.c_int)],
     "fm_device_info": [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_I64), ctypes.POINTER(_I64)],
+    "fm_device_pci_bus_id": [ctypes.c_int, ctypes.c_char_p, ctypes.c_int],
     "fm_alloc": [ctypes.POINTER(_P), _SZ, _P],
     "fm_free": [_P, _P],
     "fm_host_alloc": [ctypes.POINTER(_P), _SZ],

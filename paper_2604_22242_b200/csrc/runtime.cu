@@ -198,6 +198,11 @@ int fm_device_info(int device, int *sm, int *major, int *minor, int64_t *l2, int
   return 0;
 }
 
+int fm_device_pci_bus_id(int device, char *buf, int len) {
+  FM_CHECK(cudaDeviceGetPCIBusId(buf, len, device));
+  return 0;
+}
+
 int fm_alloc(void **ptr, size_t bytes, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (bytes == 0) bytes = 1;

@@ -142,8 +142,9 @@ class Communicator:
             raise FusematError(f"unknown transport {transport!r}")
 
     def _device_key(self):
-        from ._native import native
-        return int(self.backend.device), _pci_bus_id(native(), self.backend.device)
+        buf = ctypes.create_string_buffer(64)
+        self.nat.call("fm_device_pci_bus_id", int(self.backend.device), buf, 64)
+        return buf.value.decode()
 
     def _init_nccl(self) -> None:
         self.nat.call("fm_comm_nccl_load", (nccl_library() or "").encode() or None)
@@ -214,16 +215,6 @@ class Communicator:
         if self._comm is not None:
             self.nat.call("fm_comm_destroy", self._comm)
             self._comm = None
-
-
-def _pci_bus_id(nat, device: int) -> str:
-    """Stable identity of a device across processes (CUDA_VISIBLE_DEVICES may
-    renumber): PCI bus id through torch if present, else the ordinal."""
-    try:
-        import torch
-        return str(torch.cuda.get_device_properties(device).pci_bus_id)
-    except Exception:
-        return str(device)
 
 
 # ---------------------------------------------------------------------------------
