@@ -219,6 +219,32 @@ def cases_fixture():
     w.add("accu_small", x._node(), {x.mat_id: x.to_numpy()}, accu_ref=float(fm.accu(x)))
     big = fm.fill(2, 1, 2**31, "u32", ctx=ctx)
     w.add("accu_u32_wrap", big._node(), {big.mat_id: big.to_numpy()}, accu_ref=int(fm.accu(big)))
+    # 7. the north-star ops the reference lacks, pinned through what it HAS
+    #    (SURVEY 8c): the C4 subexpression materialised by the reference's
+    #    compiled backend, its per-column and per-row sums as the reference's
+    #    accu of Mat.submat column / row views (matrix.py:258, 481-496), and
+    #    dot / norm^2 as the reference's accu(x * y) / accu((x - y)**2).
+    #    sum / mean along a dim, max / min / index_max / index_min (numpy
+    #    semantics on the reference-computed values), dot and norm are
+    #    checked against these by tests/test_oracle.py and the GPU tests.
+    for etype, (rows, cols) in (("f64", (64, 24)), ("f64", (200, 7)), ("f32", (48, 33))):
+        ctx = fm.Context("device")
+        X, Y, Z = (fm.randu(rows, cols, s, etype, ctx) for s in (42, 43, 44))
+        e = (X - Y) * Z
+        V = fm.Mat(rows, cols, etype, ctx)
+        V.assign(e)
+        env = {m.mat_id: m.to_numpy() for m in (X, Y, Z)}
+        colsum = np.array([float(fm.accu(V.submat(0, j, rows, 1))) for j in range(cols)])
+        rowsum = np.array([float(fm.accu(V.submat(i, 0, 1, cols))) for i in range(rows)])
+        w.add(f"pin_c4_{etype}_{rows}x{cols}", e.node, env, oracle=roracle.materialize(e.node, env),
+              cjit=V.to_numpy(), colsum_ref=colsum, rowsum_ref=rowsum)
+    for etype in ("f32", "f64"):
+        ctx = fm.Context("device")
+        x, y = fm.randu(5000, 1, 7, etype, ctx), fm.randu(5000, 1, 8, etype, ctx)
+        e = (x - y) ** 2
+        env = {x.mat_id: x.to_numpy(), y.mat_id: y.to_numpy()}
+        w.add(f"pin_norm_dot_{etype}", e.node, env, normsq_ref=float(fm.accu(e)),
+              dot_ref=float(fm.accu(x * y)))
     w.save()
 
 

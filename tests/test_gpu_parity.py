@@ -126,3 +126,47 @@ def test_kernel_selection(gpu_ctx):
     z.assign(x.t() + y)
     k2 = gpu_ctx.cache.lookup("copy|" + fm.exprtree.signature_of((x.t() + y).node))
     assert k2 is not None and not k2.uses_template
+
+
+# --- north-star ops pinned through the reference -----------------------------
+def test_dim_reductions_pinned_to_reference(gpu_ctx, golden_cases):
+    """GPU sum / mean along both dims vs the reference's accu of each column /
+    row submat; max / min / index_max / index_min vs numpy on the values the
+    reference's compiled backend produced (exact)."""
+    cases, arrays = golden_cases
+    pins = [c for c in cases if c["name"].startswith("pin_c4_")]
+    assert len(pins) == 3
+    K = orc.ReduceKind
+    for c in pins:
+        node = from_json(c["tree"])
+        e = bind(node, case_env(c, arrays), gpu_ctx)
+        v = arrays[c["expected"]["cjit"]]
+        colsum = arrays[c["expected"]["colsum_ref"]]
+        rowsum = arrays[c["expected"]["rowsum_ref"]]
+        n_rows, n_cols = v.shape
+        f64 = node.etype is ElemType.f64
+        for dim, ref_sum, n in ((0, colsum, n_rows), (1, rowsum, n_cols)):
+            mag = np.abs(v.astype(np.float64)).sum(axis=dim)
+            s = fm.sum(e, dim).eval().to_numpy().ravel().astype(np.float64)
+            m = fm.mean(e, dim).eval().to_numpy().ravel().astype(np.float64)
+            if f64:
+                assert np.all(np.abs(s - ref_sum) <= 1e-13 * mag), (c["name"], dim)
+                assert np.all(np.abs(m - ref_sum / n) <= 1e-13 * mag / n), (c["name"], dim)
+            else:                     # f32 outputs: the f64 sum rounded once
+                assert np.array_equal(s.astype(np.float32), ref_sum.astype(np.float32)), (c["name"], dim)
+            for fn, red in ((fm.max, np.max), (fm.min, np.min), (fm.index_max, np.argmax),
+                            (fm.index_min, np.argmin)):
+                got = fn(e, dim).eval().to_numpy().ravel()
+                assert np.array_equal(got, red(v, axis=dim)), (c["name"], fn.__name__, dim)
+
+
+def test_norm_and_dot_pinned_to_reference(gpu_ctx, golden_cases):
+    cases, arrays = golden_cases
+    for c in (c for c in cases if c["name"].startswith("pin_norm_dot_")):
+        env = case_env(c, arrays)
+        x, y = (fm.from_array(env[k], ctx=gpu_ctx) for k in sorted(env))
+        normsq = c["expected"]["normsq_ref"]["scalar"]
+        dot = c["expected"]["dot_ref"]["scalar"]
+        assert abs(fm.norm(x - y) ** 2 - normsq) <= 1e-12 * normsq
+        assert abs(fm.dot(x, y) - dot) <= 1e-12 * dot
+        assert abs(fm.accu((x - y) ** 2) - normsq) <= 1e-12 * normsq

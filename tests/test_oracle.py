@@ -141,3 +141,52 @@ def test_ulp_metric():
     assert orc.max_ulp(a, b) == 1
     assert orc.max_ulp(np.float32([0.0]), np.float32([-0.0])) == 0
     assert math.isinf(orc.compare(np.array([np.nan]), np.array([1.0])))
+
+
+# --- north-star ops pinned through the reference ---------------------------
+def _pin_cases(golden_cases, prefix):
+    cases, arrays = golden_cases
+    return [(c, arrays) for c in cases if c["name"].startswith(prefix)]
+
+
+def test_dim_sums_pinned_to_reference_submat_accu(golden_cases):
+    """sum / mean along dim 0 and dim 1 equal the reference's own
+    accu(V.submat(...)) of each column / row (matrix.py:258, 481-496); max /
+    min / index_* follow numpy on the values the reference computed."""
+    from conftest import case_env
+    from treeio import from_json
+    cases = _pin_cases(golden_cases, "pin_c4_")
+    assert len(cases) == 3
+    for c, arrays in cases:
+        node = from_json(c["tree"])
+        v = orc.materialize(node, case_env(c, arrays))
+        ety = node.etype
+        assert np.array_equal(v, arrays[c["expected"]["cjit"]])          # exact elementwise
+        colsum = arrays[c["expected"]["colsum_ref"]]
+        rowsum = arrays[c["expected"]["rowsum_ref"]]
+        K = orc.ReduceKind
+        mag0 = np.abs(v.astype(np.float64)).sum(axis=0)
+        mag1 = np.abs(v.astype(np.float64)).sum(axis=1)
+        s0 = orc.reduce_dim(K.sum, 0, v, ety).ravel().astype(np.float64)
+        s1 = orc.reduce_dim(K.sum, 1, v, ety).ravel().astype(np.float64)
+        tol = 1e-13 if ety is orc.ElemType.f64 else 2 ** -24
+        if ety is orc.ElemType.f64:
+            assert np.all(np.abs(s0 - colsum) <= tol * mag0)
+            assert np.all(np.abs(s1 - rowsum) <= tol * mag1)
+        else:                       # f32 output: the f64 sum rounded once
+            assert np.array_equal(s0.astype(np.float32), colsum.astype(np.float32))
+            assert np.array_equal(s1.astype(np.float32), rowsum.astype(np.float32))
+        m0 = orc.reduce_dim(K.mean, 0, v, ety).ravel().astype(np.float64)
+        assert np.all(np.abs(m0 - colsum / v.shape[0]) <= max(tol, 2 ** -24) * mag0 / v.shape[0])
+
+
+def test_norm_and_dot_pinned_to_reference_accu(golden_cases):
+    from conftest import case_env
+    for c, arrays in _pin_cases(golden_cases, "pin_norm_dot_"):
+        env = case_env(c, arrays)
+        x, y = (env[k] for k in sorted(env))
+        ety = orc.ElemType.f32 if x.dtype == np.float32 else orc.ElemType.f64
+        normsq = c["expected"]["normsq_ref"]["scalar"]
+        dot = c["expected"]["dot_ref"]["scalar"]
+        assert abs(orc.accu((x - y) * (x - y), ety) - normsq) <= 1e-12 * normsq
+        assert abs(orc.accu(x * y, ety) - dot) <= 1e-12 * dot
