@@ -337,10 +337,25 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   // combine: per-CTA partials then per-chunk partials, each thread over a
   // fixed strided subset, then fixed trees
   const int64_t ndyn = nfull - dbase;
+  // The partials were written by other SMs: read them through L2 (ld.cg),
+  // kU independent loads in flight per thread, then added in the same fixed
+  // order (thread t: t, t + T, t + 2T, ...) -- the tail of the launch is
+  // these loads' latency, so they must not serialise one per add.
+  constexpr int kU = 8;
   double sd = 0.0;
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += kBulkThreads) sd = add_d(sd, ((volatile double *)part_d)[i]);
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += kBulkThreads) sd = add_d(sd, __ldcg(part_d + i));
   double sc = 0.0;
-  for (int64_t i = threadIdx.x; i < ndyn; i += kBulkThreads) sc = add_d(sc, ((volatile double *)part_c)[i]);
+  for (int64_t i0 = threadIdx.x; i0 < ndyn; i0 += (int64_t)kU * kBulkThreads) {
+    double v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + (int64_t)u * kBulkThreads;
+      v[u] = i < ndyn ? __ldcg(part_c + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + (int64_t)u * kBulkThreads < ndyn) sc = add_d(sc, v[u]);
+  }
   sd = warp_sum_d(sd);
   sc = warp_sum_d(sc);
   __shared__ double fin_d[kBulkThreads / 32], fin_c[kBulkThreads / 32];
