@@ -10,6 +10,7 @@
 #include "bulk.cuh"
 #include "skeletons.cuh"
 #include "tiled.cuh"
+#include "pair.cuh"
 
 namespace fm {
 
@@ -166,6 +167,13 @@ int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cud
     // runs directly (vector loads in load_slot)
     bool transposed = false;
     for (int j = 0; j < P.n_slots; ++j) transposed |= P.slots[j].transposed != 0;
+    // whole square matrices read plain and transposed: tile pairs, every
+    // input block staged once by TMA (pair.cuh)
+    if (transposed && pair_eligible(P, n_rows, n_cols)) {
+      bool handled = false;
+      if (int st = run_copy_pair<E>(P, out, n_rows, s, handled)) return st;
+      if (handled) return 0;
+    }
     if (tiled_enabled() && transposed && n_rows * n_cols >= 4096) return run_copy_tiled<E>(P, out, n_rows, n_cols, s);
   }
   if constexpr (E::kFast) {

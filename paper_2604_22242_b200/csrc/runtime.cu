@@ -1,5 +1,6 @@
 // runtime.cu -- device, memory, stream, event entry points of the C ABI and
 // the shared scratch / error plumbing (include/fmb200.h).
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <map>
@@ -35,6 +36,20 @@ bool pdl_enabled() {
   return on;
 }
 
+// cuTensorMapEncodeTiled from the driver through the runtime's entry-point
+// query (no link-time libcuda dependency: the CPU suite loads this library)
+void *tensor_map_encoder() {
+  static void *fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return p;
+  }();
+  return fn;
+}
+
 int sm_count() {
   static int cached[64] = {0};
   int dev = 0;
@@ -60,19 +75,62 @@ static std::map<std::pair<int, void *>, ScratchEntry> g_scratch;
 // before returning.  Used for memory whose address a CUDA graph may bake in
 // (the scratch arena, allocations made while capturing): a graph memory node
 // would be unmapped between replays and could not be relaunched unfreed.
-int alloc_plain(void **ptr, size_t bytes) {
+// per-device non-blocking side stream for the setup copies below (never
+// captured: no legacy-stream implicit synchronisation with a capture)
+static cudaError_t side_stream(int dev, cudaStream_t *out) {
   static thread_local cudaStream_t side[64] = {nullptr};
+  const int d = dev < 64 ? dev : 0;
+  if (side[d] == nullptr) {
+    cudaError_t e = cudaStreamCreateWithFlags(&side[d], cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+  }
+  *out = side[d];
+  return cudaSuccess;
+}
+
+// cudaMalloc + fill (zeros, or `host` bytes) outside any capture
+static int alloc_filled(void **ptr, size_t bytes, const void *host) {
   int dev = 0;
   FM_CHECK(cudaGetDevice(&dev));
   cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
   FM_CHECK(cudaThreadExchangeStreamCaptureMode(&mode));
+  cudaStream_t side = nullptr;
   cudaError_t e = cudaMalloc(ptr, bytes);
-  if (e == cudaSuccess && dev < 64 && side[dev] == nullptr)
-    e = cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMemsetAsync(*ptr, 0, bytes, side[dev < 64 ? dev : 0]);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(side[dev < 64 ? dev : 0]);
+  if (e == cudaSuccess) e = side_stream(dev, &side);
+  if (e == cudaSuccess)
+    e = host ? cudaMemcpyAsync(*ptr, host, bytes, cudaMemcpyHostToDevice, side) : cudaMemsetAsync(*ptr, 0, bytes, side);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(side);
   cudaThreadExchangeStreamCaptureMode(&mode);
   if (e != cudaSuccess) return fail("alloc_plain", e);
+  return 0;
+}
+
+int alloc_plain(void **ptr, size_t bytes) { return alloc_filled(ptr, bytes, nullptr); }
+
+// Tile-pair order tables (pair.cuh), one per (device, tile count); never
+// freed -- CUDA graphs may hold the address.
+int pair_order(int64_t n, const uint32_t **table) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int64_t>, void *> tables;
+  constexpr int kTile = 32, kStrip = 8;
+  int dev = 0;
+  FM_CHECK(cudaGetDevice(&dev));
+  const int64_t nt = (n + kTile - 1) / kTile;
+  std::lock_guard<std::mutex> lk(mu);
+  void *&d = tables[{dev, nt}];
+  if (d == nullptr) {
+    std::vector<uint32_t> h;
+    h.reserve((size_t)(nt * (nt + 1) / 2));
+    for (int64_t j0 = 0; j0 < nt; j0 += kStrip) {
+      const int64_t j1 = std::min<int64_t>(nt, j0 + kStrip);
+      for (int64_t i = 0; i < j1; ++i)
+        for (int64_t j = std::max(i, j0); j < j1; ++j) h.push_back((uint32_t)i | ((uint32_t)j << 16));
+    }
+    void *p = nullptr;
+    if (int st = alloc_filled(&p, h.size() * sizeof(uint32_t), h.data())) return st;
+    d = p;
+  }
+  *table = (const uint32_t *)d;
   return 0;
 }
 

@@ -65,6 +65,11 @@ struct Chunk {
   int tr = 0, tc = 0;        // chunk position inside the tile (first row, column)
   int trp = 0, tcp = 0;      // element pitches of the column-major / transposed layouts
   int slot_bytes = 0;        // bytes per staged slot
+  // tile-pair layout (pair.cuh): 0 = the per-slot layouts above; else which
+  // output tile of the pair this chunk belongs to (1: (I,J), 2: (J,I),
+  // 3: a diagonal tile), and the bytes of one staged 32 x 32 tile
+  int pair = 0;
+  int tile_bytes = 0;
 };
 
 // Load V elements of slot s for a flat chunk (every slot dense, same shape).
@@ -208,6 +213,53 @@ FM_DEV void load_staged(const fm_slot &s, const unsigned char *buf, const Chunk 
   }
 }
 
+// Load V elements of slot `s` from the tile-pair stage (pair.cuh).  Every
+// distinct buffer b (slot.reserved) has two 32 x 32 tiles staged by 2-D TMA
+// with the 128-byte swizzle: A = M[I-block, J-block] and B = M[J-block,
+// I-block], column-major, 128-byte rows (= tile columns, 16 B chunk q of
+// column c at q ^ (c & 7)); 8-byte elements take two 16-row half tiles of
+// 4 KiB.  Untransposed slots read V rows of one column (16-byte vectors);
+// transposed slots read one row across V columns of the other tile.  With
+// lane = column both patterns are bank-conflict free.
+FM_DEV int pair_off(int r, int c, int w) {
+  const int rb = r * w;
+  return ((rb >> 7) << 12) + (c << 7) + ((((rb >> 4) ^ c) & 7) << 4) + (rb & 15);
+}
+FM_DEV const unsigned char *pair_addr(const unsigned char *t, int r, int c, int w) { return t + pair_off(r, c, w); }
+template <int V>
+FM_DEV void load_pair(const fm_slot &s, const Chunk &ch, uint32_t (&lo)[V], uint32_t (&hi)[V]) {
+  const int w = s.etype == FM_F64 ? 8 : 4;
+  const int tr = s.transposed != 0;
+  const int sel = ch.pair == 3 ? 0 : (tr ^ (ch.pair == 2));
+  const unsigned char *t = ch.stage + (size_t)(s.reserved * 2 + sel) * ch.tile_bytes;
+  if (!tr) {
+    if (w == 4) {
+#pragma unroll
+      for (int q = 0; q < V / 4; ++q) {
+        const uint4 x = *(const uint4 *)pair_addr(t, ch.tr + 4 * q, ch.tc, 4);
+        lo[4 * q] = x.x; lo[4 * q + 1] = x.y; lo[4 * q + 2] = x.z; lo[4 * q + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < V / 2; ++q) {
+        const uint4 x = *(const uint4 *)pair_addr(t, ch.tr + 2 * q, ch.tc, 8);
+        lo[2 * q] = x.x; hi[2 * q] = x.y; lo[2 * q + 1] = x.z; hi[2 * q + 1] = x.w;
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const unsigned char *p = pair_addr(t, ch.tc, ch.tr + v, w);
+    if (w == 8) {
+      const uint2 x = *(const uint2 *)p;
+      lo[v] = x.x; hi[v] = x.y;
+    } else {
+      lo[v] = *(const uint32_t *)p;
+    }
+  }
+}
+
 // Slot j of the program for the chunk: staged tile when the kernel staged it
 // (every slot but diagonals), global memory otherwise.
 template <int V, bool FLAT_ONLY = false>
@@ -218,7 +270,8 @@ FM_DEV void fetch_slot(const fm_program &P, int j, const Chunk &ch, uint32_t (&l
     // carry no view / staging code: fewer live registers
     load_slot_flat<V>(s, ch, lo, hi);
   } else {
-    if (ch.stage && s.map != FM_MAP_DIAG) load_staged<V>(s, ch.stage + (size_t)j * ch.slot_bytes, ch, lo, hi);
+    if (ch.pair) load_pair<V>(s, ch, lo, hi);
+    else if (ch.stage && s.map != FM_MAP_DIAG) load_staged<V>(s, ch.stage + (size_t)j * ch.slot_bytes, ch, lo, hi);
     else load_slot<V>(s, ch, lo, hi);
   }
 }

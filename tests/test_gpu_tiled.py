@@ -140,3 +140,114 @@ def test_bf16_transposed_leaf(ctx):
     Z.assign(fm.conv_to(X.t(), "f32") + Y)
     want = X.to_numpy().astype(np.float32).T + Y.to_numpy()
     assert np.array_equal(Z.to_numpy(), want)
+
+
+# ---- tile pairs (csrc/pair.cuh): whole square matrices read plain and
+# transposed; each CTA stages blocks (I,J) and (J,I) of every distinct buffer
+# once by 2-D TMA.  Edge sizes: exactly one tile, a ragged last tile, the
+# smallest eligible size, and shapes that fall back to the per-slot path.
+
+@pytest.mark.parametrize("etype", ["f32", "f64"])
+@pytest.mark.parametrize("n", [32, 36, 64, 100, 2052])
+def test_pair_expr1_edges(ctx, n, etype):
+    X, Y, x, y = _pair(ctx, (n, n), etype, 3)
+    Z = fm.zeros(n, n, etype, ctx)
+    Z.assign(2 * (X.t() + Y) + 2 * (X + Y.t()))
+    t = x.dtype.type(2)
+    assert np.array_equal(Z.to_numpy(), t * (x.T + y) + t * (x + y.T))
+
+
+@pytest.mark.parametrize("n", [33, 31, 34])
+def test_pair_ineligible_sizes_fall_back(ctx, n):
+    """n*4 not a 16-byte multiple (TMA strides) or below one tile."""
+    X, Y, x, y = _pair(ctx, (n, n), "f32", 4)
+    Z = fm.zeros(n, n, ctx=ctx)
+    Z.assign(X.t() - Y * X)
+    assert np.array_equal(Z.to_numpy(), x.T - y * x)
+
+
+@pytest.mark.parametrize("etype", ["f32", "f64"])
+def test_pair_expr2(ctx, etype):
+    """Paper expr2: a*A + (B + C).t() + log(D**2) -- four buffers, two transposed."""
+    n = 1000
+    ms = [fm.randu(n, n, 70 + i, etype, ctx) for i in range(4)]
+    a, b, c, d = ms
+    Z = fm.zeros(n, n, etype, ctx)
+    Z.assign(0.5 * a + (b + c).t() + fm.log(d ** 2))
+    av, bv, cv, dv = (m.to_numpy() for m in ms)
+    T = av.dtype.type
+    lg = np.log((dv * dv).astype(np.float64))
+    want = (T(0.5) * av + (bv + cv).T) + (lg.astype(av.dtype) if etype == "f32" else lg)
+    if etype == "f32":       # f32 log correctly rounded (via f64): <= 1 ulp
+        assert orc.max_ulp(Z.to_numpy(), want) <= 1
+    else:                    # f64 transcendentals: 1e-12 relative (DESIGN.md numerics),
+        z = Z.to_numpy()     # against max(|want|, 1): the sum can cancel to ~0
+        assert np.max(np.abs(z - want) / np.maximum(np.abs(want), 1.0)) <= 1e-12
+
+
+def test_pair_transposed_only_and_self(ctx):
+    """X.t() alone, X.t() * X (one buffer, both blocks), X.t() % X.t()."""
+    n = 640
+    X = fm.randu(n, n, 81, "f32", ctx)
+    x = X.to_numpy()
+    Z = fm.zeros(n, n, ctx=ctx)
+    Z.assign(X.t() + 0.0)
+    assert np.array_equal(Z.to_numpy(), x.T + np.float32(0))
+    Z.assign(X.t() % X - X)
+    assert np.array_equal(Z.to_numpy(), x.T * x - x)
+    Z.assign(X.t() % X.t())
+    assert np.array_equal(Z.to_numpy(), x.T * x.T)
+
+
+def test_pair_mixed_widths(ctx):
+    """f64 program with an f32 and a u32 leaf (4- and 8-byte tiles in one stage)."""
+    n = 520
+    A = fm.randu(n, n, 90, "f64", ctx)
+    B = fm.randu(n, n, 91, "f32", ctx)
+    U = fm.randi(n, n, 7, 92, "u32", ctx)
+    Z = fm.zeros(n, n, "f64", ctx)
+    Z.assign(A.t() * fm.conv_to(B, "f64") + fm.conv_to(U.t(), "f64") - A)
+    a, b, u = A.to_numpy(), B.to_numpy(), U.to_numpy()
+    want = (a.T * b.astype(np.float64) + u.T.astype(np.float64)) - a
+    assert np.array_equal(Z.to_numpy(), want)
+
+
+def test_pair_many_buffers_falls_back(ctx):
+    """More distinct buffers than the pair kernel stages (8): per-slot path."""
+    n = 256
+    ms = [fm.randu(n, n, 100 + i, "f32", ctx) for i in range(10)]
+    e = ms[0].t()
+    for m in ms[1:]:
+        e = e + m
+    Z = fm.zeros(n, n, ctx=ctx)
+    Z.assign(e)
+    want = ms[0].to_numpy().T
+    for m in ms[1:]:
+        want = want + m.to_numpy()
+    assert np.array_equal(Z.to_numpy(), want)
+
+
+def test_pair_result_into_u32_and_graph_replay(ctx):
+    """Integer program on the pair path, captured in a CUDA graph and replayed."""
+    n = 300
+    U = fm.randi(n, n, 1000, 5, "u32", ctx)
+    V = fm.randi(n, n, 1000, 6, "u32", ctx)
+    Z = fm.zeros(n, n, "u32", ctx)
+    g = fm.capture(lambda: Z.assign(U.t() + V * U), ctx)
+    Z.assign(U * 0)
+    g.replay()
+    g.replay()
+    ctx.sync()
+    u, v = U.to_numpy(), V.to_numpy()
+    assert np.array_equal(Z.to_numpy(), u.T + v * u)
+
+
+@pytest.mark.parametrize("etype", ["f32", "f64"])
+def test_pair_in_place(ctx, etype):
+    """Z = Z + Y.t() (a SAFE alias: every block of Z is read and written by the one CTA that owns its pair)."""
+    n = 1000
+    Z = fm.randu(n, n, 11, etype, ctx)
+    Y = fm.randu(n, n, 12, etype, ctx)
+    z, y = Z.to_numpy(), Y.to_numpy()
+    Z.assign(Z + Y.t())
+    assert np.array_equal(Z.to_numpy(), z + y.T)
