@@ -110,17 +110,7 @@ int launch_tiled(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols,
   }
   const int64_t ntiles = cdiv(n_rows, G::TR) * cdiv(n_cols, TC);
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sm_count() * occ_blocks));
-  // square tiles on a square grid could schedule (I,J) next to (J,I) for L2
-  // reuse of the blocks a transposed leaf and its untransposed twin both read;
-  // measured slower (expr1 f64 8192^2: 2.35 paired vs 2.56 TB/s in column
-  // order, which keeps consecutive CTAs on neighbouring HBM pages), so it is
-  // opt-in: FMB200_TILED_PAIR=1.
-  static const int pair_env = [] {
-    const char *e = getenv("FMB200_TILED_PAIR");
-    return (e && *e) ? atoi(e) : 0;
-  }();
-  const int paired = (pair_env && G::TR == TC && n_rows == n_cols) ? 1 : 0;
-  tiled::k_copy_tiled<E, TC><<<(unsigned)grid, G::NT, smem, s>>>(P, out, n_rows, n_cols, paired);
+  tiled::k_copy_tiled<E, TC><<<(unsigned)grid, G::NT, smem, s>>>(P, out, n_rows, n_cols);
   FM_CHECK_LAUNCH("fused copy kernel (tiled)");
   return 0;
 }
@@ -128,18 +118,8 @@ int launch_tiled(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols,
 template <class E>
 int run_copy_tiled(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s) {
   constexpr int64_t kMaxSmem = 200 * 1024;
-  // square 64 x 64 tiles (V = 8) for square domains would let tile pairing
-  // apply, but 512-thread CTAs at one per SM lose more than the L2 reuse
-  // gains (expr1 at 10000^2: 2.17 vs 2.77 TB/s) -- opt in with
-  // FMB200_TILED_SQUARE=1.  (f64, V = 4, tiles are square already.)
-  if constexpr (E::kV == 8) {
-    static const int sq = [] {
-      const char *e = getenv("FMB200_TILED_SQUARE");
-      return (e && *e) ? atoi(e) : 0;
-    }();
-    if (sq && n_rows == n_cols && tiled::smem_bytes<E, 64>(P.n_slots) <= kMaxSmem)
-      return launch_tiled<E, 64>(P, out, n_rows, n_cols, s);
-  }
+  // (whole square matrices with transposed leaves take the tile-pair
+  // skeleton, pair.cuh, before this)
   if (tiled::smem_bytes<E, 32>(P.n_slots) <= kMaxSmem) return launch_tiled<E, 32>(P, out, n_rows, n_cols, s);
   if (tiled::smem_bytes<E, 16>(P.n_slots) <= kMaxSmem) return launch_tiled<E, 16>(P, out, n_rows, n_cols, s);
   return launch_tiled<E, 8>(P, out, n_rows, n_cols, s);

@@ -371,7 +371,9 @@ void *tensor_map_encoder();   // runtime.cu: cuTensorMapEncodeTiled via the runt
 // tensor map per buffer.  Returns false when the program has more distinct
 // buffers than the kernel stages.
 // one 2-D tensor map over an n x n column-major matrix of w-byte elements,
-// box {128 bytes of a column, 32 columns}, 128-byte swizzle
+// box {128 bytes of a column, 32 columns}, 128-byte swizzle; 64-byte L2
+// promotion (r02, scripts/gpu_promo.sh: neutral on aligned n, +6 % at
+// n = 10000 f32 where odd columns start mid-line; 256 B costs up to 10 %)
 inline int pair_encode(CUtensorMap *map, const void *ptr, int64_t n, int w) {
   EncodeTiledFn enc = (EncodeTiledFn)tensor_map_encoder();
   if (!enc) return fail_msg("pair: cuTensorMapEncodeTiled unavailable from the driver");
@@ -381,7 +383,7 @@ inline int pair_encode(CUtensorMap *map, const void *ptr, int64_t n, int w) {
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, w == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
                    const_cast<void *>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_64B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail_msg("pair: cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
   return 0;
 }

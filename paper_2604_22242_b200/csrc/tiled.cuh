@@ -115,30 +115,16 @@ FM_DEV void stage_tile(const fm_program &P, unsigned char *buf, int64_t r0, int6
   }
 }
 
-// Tile t -> (row block, column block).  Paired order (square tiles on a
-// square grid): tiles (I,J) and (J,I) are consecutive, so CTAs running at the
-// same time stage both -- the block a transposed leaf reads for (I,J) is the
-// block the untransposed leaf of the same matrix reads for (J,I), and the
-// second read hits L2 instead of HBM.  Group J holds (0,J),(J,0),(1,J),(J,1),
-// ..., (J,J); it starts at tile J^2.
-FM_DEV void tile_of(int64_t t, int64_t ntr, bool paired, int64_t &bi, int64_t &bj) {
-  if (!paired) {
-    bi = t % ntr;
-    bj = t / ntr;
-    return;
-  }
-  int64_t J = (int64_t)sqrt((double)t);
-  while (J * J > t) --J;
-  while ((J + 1) * (J + 1) <= t) ++J;
-  const int64_t u = t - J * J;
-  if (u == 2 * J) { bi = J; bj = J; return; }
-  const int64_t I = u >> 1;
-  if (u & 1) { bi = J; bj = I; } else { bi = I; bj = J; }
+// Tile t -> (row block, column block), column-major tile order (neighbouring
+// CTAs on neighbouring HBM pages).
+FM_DEV void tile_of(int64_t t, int64_t ntr, int64_t &bi, int64_t &bj) {
+  bi = t % ntr;
+  bj = t / ntr;
 }
 
 template <class E, int TC>
 __global__ void __launch_bounds__(8 * TC) k_copy_tiled(const __grid_constant__ fm_program P, void *out,
-                                                        int64_t n_rows, int64_t n_cols, int paired) {
+                                                        int64_t n_rows, int64_t n_cols) {
   constexpr int V = E::kV, WMAX = E::kWide ? 8 : 4;
   using G = Geo<V, TC, WMAX>;
   extern __shared__ __align__(16) unsigned char sm[];
@@ -149,7 +135,7 @@ __global__ void __launch_bounds__(8 * TC) k_copy_tiled(const __grid_constant__ f
   int64_t t = blockIdx.x;
   if (t < ntiles) {
     int64_t bi, bj;
-    tile_of(t, ntr, paired != 0, bi, bj);
+    tile_of(t, ntr, bi, bj);
     const int64_t r0 = bi * G::TR, c0 = bj * TC;
     stage_tile<V, TC, WMAX>(P, sm, r0, c0, (int)min((int64_t)G::TR, n_rows - r0), (int)min((int64_t)TC, n_cols - c0));
   }
@@ -158,7 +144,7 @@ __global__ void __launch_bounds__(8 * TC) k_copy_tiled(const __grid_constant__ f
     const int64_t tn = t + gridDim.x;
     if (tn < ntiles) {
       int64_t bi, bj;
-      tile_of(tn, ntr, paired != 0, bi, bj);
+      tile_of(tn, ntr, bi, bj);
       const int64_t r0 = bi * G::TR, c0 = bj * TC;
       stage_tile<V, TC, WMAX>(P, sm + (b ^ 1) * buf_bytes, r0, c0, (int)min((int64_t)G::TR, n_rows - r0),
                         (int)min((int64_t)TC, n_cols - c0));
@@ -167,7 +153,7 @@ __global__ void __launch_bounds__(8 * TC) k_copy_tiled(const __grid_constant__ f
     cp_wait<1>();        // this tile's copies (all but the newest group) have landed
     __syncthreads();
     int64_t bi, bj;
-    tile_of(t, ntr, paired != 0, bi, bj);
+    tile_of(t, ntr, bi, bj);
     const int64_t r0 = bi * G::TR, c0 = bj * TC;
     const int rv = (int)min((int64_t)G::TR, n_rows - r0), cv = (int)min((int64_t)TC, n_cols - c0);
     if (cc < cv && k * V < rv) {
