@@ -840,15 +840,20 @@ class Suite(Config):
         from paper_2604_22242_b200.plan import plan
         fm, ctx = self.fm, self.ctx
         n = self.n = run.size("suite") or 10000
-        self.workload = f"paper suite (13 expressions) + addN sweep (N = 2..64), f32 {n}x{n}"
+        self.workload = f"paper suite (13 expressions incl. the 3-GEMM chain) + addN sweep (N = 2..64), f32 {n}x{n}"
         R = lambda k: fm.randu(n, n, 42 + k, "f32", ctx)  # noqa: E731
         a, b, c, dd = R(0), R(1), R(2), R(3)
         self.a, self.b = a, b
         u = fm.randi(n, n, 10, 43, "u32", ctx)
         half = n // 2
+        # chain (reference bench.py:109-117): 4 matrices of decreasing sizes,
+        # n x n/2, n/2 x n/4, n/4 x n/8, n/8 x n/16, multiplied left to right
+        d = [max(n // (2 ** i), 1) for i in range(5)]
+        ch = [fm.randu(d[i], d[i + 1], 42 + 70 + i, "f32", ctx) for i in range(4)]
         exprs = {
             "add2": (a + b, (n, n)),
             "add4": (a + b + c + dd, (n, n)),
+            "chain": (ch[0] @ ch[1] @ ch[2] @ ch[3], (d[0], d[4])),
             "addsub2": (a.center_half() + b.center_half(), (half, half)),
             "addsub4": (a.center_half() + b.center_half() + c.center_half() + dd.center_half(), (half, half)),
             "expr1": (2 * (a.t() + b) + 2 * (a + b.t()), (n, n)),
@@ -895,9 +900,19 @@ class Suite(Config):
 def plan_bytes(pl) -> int:
     """Algorithmic bytes of a plan (reference bench.py:218-240 convention);
     temps written and re-read between split launches count as traffic."""
-    from paper_2604_22242_b200.plan import FusedKernelStep
+    from paper_2604_22242_b200.plan import FusedKernelStep, GemmStep
     total = 0
     for step in pl.steps:
+        if isinstance(step, GemmStep):
+            # reference: (left + right + out) elements of the product step; an
+            # operand prologue reads its expression's inputs instead
+            for sid, shape, expr in ((step.a_id, step.a_shape, step.a_expr), (step.b_id, step.b_shape, step.b_expr)):
+                if expr is None:
+                    total += shape.n_elem * step.in_etype.width
+                else:
+                    total += sum(sp.parent_shape.n_elem * sp.etype.width for sp in expr.inputs)
+            total += step.out_shape.n_elem * step.out_etype.width
+            continue
         if not isinstance(step, FusedKernelStep):
             continue
         for spec in step.inputs:

@@ -203,6 +203,14 @@ int fm_launch_reduce_dim(int kernel_id, const fm_program *prog, int32_t dim,
                          const fm_reduce_out *outs, int32_t n_outs, void *stream);
 
 int fm_gemm(const fm_gemm_args *args, void *stream);
+/* GEMM whose operand A and/or B is an elementwise expression (a MatMul-free
+ * fused program over the operand's stored shape, rows = lda) instead of a
+ * buffer -- the operand prologue.  The reference materialises such operands
+ * into temps first (plan.py:125-151); on the f32 tensor path the program is
+ * evaluated straight into the GEMM's bf16 operand planes.  NULL programs
+ * read args->a / args->b as fm_gemm does. */
+int fm_gemm_prologue(const fm_gemm_args *args, const fm_program *a_prog, const fm_program *b_prog,
+                     void *stream);
 /* which kernel fm_gemm would run for these arguments, without launching:
  * FM_GEMM_PATH_EXACT (SIMT, f64 accumulation) or FM_GEMM_PATH_TCGEN05 */
 enum { FM_GEMM_PATH_EXACT = 0, FM_GEMM_PATH_TCGEN05 = 1 };

@@ -113,6 +113,7 @@ SIGNATURES = {
                              ctypes.POINTER(FmReduceOut), _I32, _P],
     "fm_gemm": [ctypes.POINTER(FmGemmArgs), _P],
     "fm_gemm_plan": [ctypes.POINTER(FmGemmArgs), ctypes.POINTER(ctypes.c_int)],
+    "fm_gemm_prologue": [ctypes.POINTER(FmGemmArgs), ctypes.POINTER(FmProgram), ctypes.POINTER(FmProgram), _P],
     "fm_randu": [_P, _I32, _I64, ctypes.c_uint64, _I64, _P],
     "fm_randi": [_P, _I32, _I64, ctypes.c_uint32, ctypes.c_uint64, _I64, _P],
     "fm_fill": [_P, _I32, _I64, ctypes.c_uint64, _P],

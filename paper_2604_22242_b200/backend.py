@@ -432,6 +432,19 @@ class B200Backend(Backend):
             prog.scalars[spec.index] = lw.scalar_bits(args[kernel.scalar_pos[spec.index]], spec.cls)
         return prog
 
+    def bind(self, kernel: CompiledKernel, args: list) -> FmProgram:
+        """The kernel's program bound to `args` (memoised like `launch`)."""
+        key = _memo_key(args)
+        memo = getattr(kernel, "_memo", None)
+        if memo is not None and memo[0] == key:
+            for a in args:
+                if isinstance(a, BufferHandle) and (a.id in self._freed or a.id not in self._ptrs):
+                    raise BackendError(f"use after free of buffer {a.id}")
+            return memo[1]
+        prog = self._bind(kernel, args)
+        kernel._memo = (key, prog)
+        return prog
+
     def launch(self, kernel: CompiledKernel, args: list, geometry: tuple[int, int],
                reduce_outputs=None) -> None:
         n_rows, n_cols = int(args[1]), int(args[2])
@@ -479,25 +492,33 @@ class B200Backend(Backend):
 
     # -- linear algebra --------------------------------------------------------------------
 
-    def _gemm_args(self, out: BufferHandle, a: BufferHandle, b: BufferHandle, m: int, n: int, k: int,
-                   trans_a: bool, trans_b: bool, alpha: float, lda: int | None, ldb: int | None,
+    def _gemm_args(self, out: BufferHandle, a: BufferHandle | None, b: BufferHandle | None, m: int, n: int,
+                   k: int, trans_a: bool, trans_b: bool, alpha: float, lda: int | None, ldb: int | None,
                    precision: int, c_in: BufferHandle | None = None, alpha2: float = 1.0,
-                   beta: float = 0.0) -> FmGemmArgs:
-        if a.etype is not b.etype or not a.etype.is_float:
+                   beta: float = 0.0, in_etype: ElemType | None = None) -> FmGemmArgs:
+        """`a` / `b` None: that operand is a prologue program (its type is
+        `in_etype`)."""
+        et = {h.etype for h in (a, b) if h is not None}
+        if in_etype is not None:
+            et.add(ElemType.of(in_etype))
+        if len(et) != 1 or not next(iter(et)).is_float:
             raise BackendError("gemm operands must share a float element type")
+        etype = next(iter(et))
         args = FmGemmArgs()
-        args.a, args.b, args.c = self.ptr(a), self.ptr(b), self.ptr(out)
+        args.a = self.ptr(a) if a is not None else None
+        args.b = self.ptr(b) if b is not None else None
+        args.c = self.ptr(out)
         args.lda = lda if lda is not None else (k if trans_a else m)
         args.ldb = ldb if ldb is not None else (n if trans_b else k)
         args.ldc = m
         args.trans_a, args.trans_b = int(trans_a), int(trans_b)
         args.m, args.n, args.k = m, n, k
         args.alpha = alpha
-        args.in_etype = a.etype.code
+        args.in_etype = etype.code
         args.out_etype = out.etype.code
         args.precision = precision
         need_a, need_b = args.lda * (m if trans_a else k), args.ldb * (k if trans_b else n)
-        if a.n_elem < need_a or b.n_elem < need_b or out.n_elem < m * n:
+        if (a is not None and a.n_elem < need_a) or (b is not None and b.n_elem < need_b) or out.n_elem < m * n:
             raise BackendError("gemm buffer smaller than its operand")
         args.alpha2, args.beta = alpha2, beta
         if c_in is not None:
@@ -506,16 +527,27 @@ class B200Backend(Backend):
             args.c_in, args.ld_c_in = self.ptr(c_in), m
         return args
 
-    def gemm(self, out: BufferHandle, a: BufferHandle, b: BufferHandle, m: int, n: int, k: int,
+    def gemm(self, out: BufferHandle, a: BufferHandle | None, b: BufferHandle | None, m: int, n: int, k: int,
              trans_a: bool = False, trans_b: bool = False, alpha: float = 1.0,
              lda: int | None = None, ldb: int | None = None, precision: int = 0,
-             c_in: BufferHandle | None = None, alpha2: float = 1.0, beta: float = 0.0) -> None:
+             c_in: BufferHandle | None = None, alpha2: float = 1.0, beta: float = 0.0,
+             a_prog: FmProgram | None = None, b_prog: FmProgram | None = None,
+             in_etype: ElemType | None = None) -> None:
         """out = alpha * op(a) @ op(b), or with an addend
         out = alpha2 * (alpha * op(a) @ op(b)) + beta * c_in (each product and
-        the sum rounded to the output type)."""
+        the sum rounded to the output type).  An operand given as a bound
+        program (`a_prog` / `b_prog`, its buffer None) is that elementwise
+        expression over the operand's stored shape (fm_gemm_prologue)."""
+        if (a is None) != (a_prog is not None) or (b is None) != (b_prog is not None):
+            raise BackendError("each gemm operand is a buffer or a prologue program")
         args = self._gemm_args(out, a, b, m, n, k, trans_a, trans_b, alpha, lda, ldb, precision,
-                               c_in, alpha2, beta)
-        self.nat.call("fm_gemm", ctypes.byref(args), self.stream)
+                               c_in, alpha2, beta, in_etype)
+        if a_prog is None and b_prog is None:
+            self.nat.call("fm_gemm", ctypes.byref(args), self.stream)
+        else:
+            self.nat.call("fm_gemm_prologue", ctypes.byref(args),
+                          ctypes.byref(a_prog) if a_prog is not None else None,
+                          ctypes.byref(b_prog) if b_prog is not None else None, self.stream)
         self.launch_count += 1
 
     def gemm_path(self, out: BufferHandle, a: BufferHandle, b: BufferHandle, m: int, n: int, k: int,

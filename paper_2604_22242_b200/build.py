@@ -39,7 +39,7 @@ def units() -> list[tuple[str, str, list[str]]]:
     from .aot_registry import TEMPLATE_SHARDS
     out = [(Path(s).stem, s, []) for s in SOURCES]
     for v in range(4):
-        for k in range(3):
+        for k in range(4):
             out.append((f"vm_inst_{v}_{k}", "vm_inst.cu", [f"-DFM_VM_VARIANT={v}", f"-DFM_VM_SKELETON={k}"]))
     for k in range(TEMPLATE_SHARDS):
         out.append((f"gen_templates_{k}", "gen_templates.cu",

@@ -31,6 +31,14 @@ int alloc_plain(void **ptr, size_t bytes);
 
 int sm_count();
 
+// fused.cu: run a validated program through the generic (VM) kernels --
+// the GEMM operand prologue (split into bf16 planes, split.cuh) or a plain
+// copy into a buffer (operands of the exact GEMM path)
+int validate_program(const fm_program *P);
+int launch_split_program(const fm_program &P, uint16_t *planes, int64_t n_rows, int64_t n_cols, int64_t ld_out,
+                         int64_t plane_off, cudaStream_t s);
+int launch_copy_program(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s);
+
 // Programmatic dependent launch: kernels launched through launch_pdl may
 // start while the previous kernel on the stream drains; they call
 // pdl_wait() before touching global memory (it returns once the previous

@@ -13,7 +13,7 @@
 
 namespace fm {
 
-static int validate(const fm_program *P) {
+int validate_program(const fm_program *P) {
   if (!P) return fail_msg("null program");
   if (P->n_instr <= 0 || P->n_instr > FM_MAX_INSTR) return fail_msg("program: bad instruction count");
   if (P->n_slots < 0 || P->n_slots > FM_MAX_SLOTS) return fail_msg("program: bad slot count");
@@ -56,6 +56,20 @@ template <class E> struct DimF {
     return run_reduce_dim<E>(P, dim, r, c, R, s);
   }
 };
+
+template <class E> struct SplitF {
+  static int run(const fm_program &P, uint16_t *o, int64_t r, int64_t c, int64_t ld, int64_t po, cudaStream_t s) {
+    return run_split<E>(P, o, r, c, ld, po, s);
+  }
+};
+
+int launch_split_program(const fm_program &P, uint16_t *planes, int64_t n_rows, int64_t n_cols, int64_t ld_out,
+                         int64_t plane_off, cudaStream_t s) {
+  return vm_dispatch<SplitF>(P, planes, n_rows, n_cols, ld_out, plane_off, s);
+}
+int launch_copy_program(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s) {
+  return vm_dispatch<CopyF>(P, out, n_rows, n_cols, s);
+}
 
 static const TemplateEntry *entry_for(int kernel_id, int skeleton) {
   if (kernel_id < 0) return nullptr;
@@ -116,7 +130,7 @@ int fm_kernel_lookup(const char *qsig, int *kernel_id) {
 
 int fm_launch_copy(int kernel_id, const fm_program *prog, void *out, int64_t n_rows, int64_t n_cols,
                    void *stream) {
-  int st = validate(prog);
+  int st = validate_program(prog);
   if (st) return st;
   if (!out && n_rows * n_cols > 0) return fail_msg("copy: null output");
   cudaStream_t s = (cudaStream_t)stream;
@@ -130,7 +144,7 @@ int fm_launch_copy(int kernel_id, const fm_program *prog, void *out, int64_t n_r
 
 int fm_launch_accu(int kernel_id, const fm_program *prog, void *out, int64_t n_rows, int64_t n_cols,
                    int32_t finalize, void *stream) {
-  int st = validate(prog);
+  int st = validate_program(prog);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if (kernel_id >= 0) {
@@ -143,7 +157,7 @@ int fm_launch_accu(int kernel_id, const fm_program *prog, void *out, int64_t n_r
 
 int fm_launch_reduce_dim(int kernel_id, const fm_program *prog, int32_t dim, int64_t n_rows,
                          int64_t n_cols, const fm_reduce_out *outs, int32_t n_outs, void *stream) {
-  int st = validate(prog);
+  int st = validate_program(prog);
   if (st) return st;
   if (dim != 0 && dim != 1) return fail_msg("reduce_dim: dim must be 0 or 1");
   if (n_outs <= 0 || n_outs > FM_MAX_REDUCE_OUT) return fail_msg("reduce_dim: bad output count");

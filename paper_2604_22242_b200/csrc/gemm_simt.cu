@@ -93,7 +93,8 @@ int gemm_exact(const fm_gemm_args &g, cudaStream_t s) {
 }
 
 // defined in gemm_tc.cu
-int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled);
+int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled, const fm_program *a_prog = nullptr,
+                const fm_program *b_prog = nullptr);
 bool gemm_tensor_supported(const fm_gemm_args &g);
 
 }  // namespace fm
@@ -141,4 +142,50 @@ extern "C" int fm_gemm(const fm_gemm_args *args, void *stream) {
     if (g.precision == FM_GEMM_TENSOR) return fail_msg("gemm: shape not supported by the tensor-core kernel");
   }
   return gemm_exact(g, s);
+}
+
+// GEMM with elementwise operand prologues (include/fmb200.h): operand A (B)
+// is the value of `a_prog` (`b_prog`) over its stored shape instead of the
+// buffer g.a (g.b).  On the f32 tensor path the expression is evaluated into
+// the bf16 operand planes the GEMM reads anyway (split.cuh) -- no operand
+// temp; elsewhere (exact / f64 / bf16 paths) it is materialised into a
+// stream-ordered temp first, exactly the reference's plan (plan.py:125-151).
+extern "C" int fm_gemm_prologue(const fm_gemm_args *args, const fm_program *a_prog, const fm_program *b_prog,
+                                void *stream) {
+  if (!args) return fail_msg("gemm: null args");
+  if (!a_prog && !b_prog) return fm_gemm(args, stream);
+  fm_gemm_args g = *args;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t ar = g.trans_a ? g.k : g.m, ac = g.trans_a ? g.m : g.k;
+  const int64_t br = g.trans_b ? g.n : g.k, bc = g.trans_b ? g.k : g.n;
+  for (const fm_program *P : {a_prog, b_prog}) {
+    if (!P) continue;
+    if (int st = validate_program(P)) return st;
+    if (P->result_etype != g.in_etype) return fail_msg("gemm prologue: expression type differs from the operand type");
+  }
+  if (a_prog) g.lda = ar;
+  if (b_prog) g.ldb = br;
+  if (g.m == 0 || g.n == 0 || g.k == 0) return fm_gemm(&g, stream);
+  if (g.in_etype == FM_F32 && use_tensor(g)) {
+    bool handled = false;
+    int st = gemm_tensor(g, s, &handled, a_prog, b_prog);
+    if (st || handled) return st;
+  }
+  const size_t w = g.in_etype == FM_F64 ? 8 : (g.in_etype == FM_BF16 ? 2 : 4);
+  void *ta = nullptr, *tb = nullptr;
+  int st = 0;
+  if (a_prog) {
+    FM_CHECK(cudaMallocAsync(&ta, (size_t)(ar * ac) * w, s));
+    st = launch_copy_program(*a_prog, ta, ar, ac, s);
+    g.a = ta;
+  }
+  if (!st && b_prog) {
+    cudaError_t e = cudaMallocAsync(&tb, (size_t)(br * bc) * w, s);
+    st = e == cudaSuccess ? launch_copy_program(*b_prog, tb, br, bc, s) : fail("cudaMallocAsync", e);
+    g.b = tb;
+  }
+  if (!st) st = fm_gemm(&g, stream);
+  if (ta) cudaFreeAsync(ta, s);
+  if (tb) cudaFreeAsync(tb, s);
+  return st;
 }

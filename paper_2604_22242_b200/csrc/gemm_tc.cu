@@ -28,6 +28,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "ops.cuh"
 
 namespace fm {
 namespace tc {
@@ -589,18 +590,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTc, 1)
   }
 }
 
-// f32 -> three bf16 planes with x = hi + mid + lo + O(2^-24 |x|): each
-// residual is exact in f32 (Sterbenz), each plane the round-to-nearest bf16
-// of the residual.  Plane p of element (i, j) goes to out[p*plane_off + i + j*ld_out].
-__device__ __forceinline__ void split3(float x, uint16_t &h, uint16_t &m, uint16_t &l) {
-  const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-  const float r1 = __fsub_rn(x, __bfloat162float(hi));
-  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-  const float r2 = __fsub_rn(r1, __bfloat162float(mid));
-  h = __bfloat16_as_ushort(hi);
-  m = __bfloat16_as_ushort(mid);
-  l = __bfloat16_as_ushort(__float2bfloat16_rn(r2));
-}
+// split3 (ops.cuh): f32 -> three bf16 planes
 
 // Grid: x over row runs of 4 elements, y over columns (no per-element
 // division); 16-byte loads and 8-byte stores per plane when the column runs
@@ -701,7 +691,7 @@ struct Planes {
   uint64_t inner = 0, outer = 0, ld = 0;
 };
 int split_operand(const float *src, int64_t rows, int64_t cols, int64_t ld_in, bool k_is_cols, int64_t kplane,
-                  Planes *pl, cudaStream_t s) {
+                  Planes *pl, cudaStream_t s, const fm_program *prog) {
   int64_t ld_out, plane_off, bytes;
   if (k_is_cols) {   // MN-major operand: planes appended along the column (K) dimension
     ld_out = round_up(rows, 8);
@@ -718,6 +708,8 @@ int split_operand(const float *src, int64_t rows, int64_t cols, int64_t ld_in, b
   FM_CHECK(cudaMallocAsync((void **)&pl->buf, (size_t)bytes, s));
   const int64_t kdim = k_is_cols ? cols : rows;
   if (kdim != kplane) FM_CHECK(cudaMemsetAsync(pl->buf, 0, (size_t)bytes, s));   // zero K padding
+  if (prog)   // operand prologue: the operand's expression evaluated into the planes (split.cuh)
+    return launch_split_program(*prog, pl->buf, rows, cols, ld_out, plane_off, s);
   const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 1023) / 1024, 64));
   const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cols, 65535));
   tc::k_split3<<<dim3(gx, gy), 256, 0, s>>>(src, rows, cols, ld_in, pl->buf, ld_out, plane_off);
@@ -726,10 +718,12 @@ int split_operand(const float *src, int64_t rows, int64_t cols, int64_t ld_in, b
 }
 }  // namespace
 
-int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
+int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled, const fm_program *a_prog,
+                const fm_program *b_prog) {
   using namespace tc;
   *handled = false;
   if (!gemm_tensor_supported(g)) return 0;
+  if ((a_prog || b_prog) && g.in_etype != FM_F32) return 0;   // prologues ride on the f32 operand split
   Params p;
   p.c = (float *)g.c;
   p.ldc = g.ldc;
@@ -772,11 +766,11 @@ int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled) {
     const uint32_t A[6] = {0, 1, 2, 0, 1, 0}, B[6] = {2, 1, 0, 1, 0, 0};
     p.pa = p.pb = 0;
     for (int i = 0; i < 6; ++i) { p.pa |= A[i] << (3 * i); p.pb |= B[i] << (3 * i); }
-    st = p.a_mn ? split_operand((const float *)g.a, g.m, g.k, g.lda, true, kplane, &pa, s)
-                : split_operand((const float *)g.a, g.k, g.m, g.lda, false, kplane, &pa, s);
+    st = p.a_mn ? split_operand((const float *)g.a, g.m, g.k, g.lda, true, kplane, &pa, s, a_prog)
+                : split_operand((const float *)g.a, g.k, g.m, g.lda, false, kplane, &pa, s, a_prog);
     if (st) return st;
-    st = p.b_mn ? split_operand((const float *)g.b, g.n, g.k, g.ldb, true, kplane, &pb, s)
-                : split_operand((const float *)g.b, g.k, g.n, g.ldb, false, kplane, &pb, s);
+    st = p.b_mn ? split_operand((const float *)g.b, g.n, g.k, g.ldb, true, kplane, &pb, s, b_prog)
+                : split_operand((const float *)g.b, g.k, g.n, g.ldb, false, kplane, &pb, s, b_prog);
     if (st) { cudaFreeAsync(pa.buf, s); return st; }
     st = encode_map(&ma, pa.buf, pa.inner, pa.outer, pa.ld, p.a_mn ? 64 : BK, p.a_mn ? BK : BM);
     if (!st) st = encode_map(&mb, pb.buf, pb.inner, pb.outer, pb.ld, p.b_mn ? 64 : BK, p.b_mn ? BK : b_box_rows);

@@ -296,3 +296,5 @@ struct TemplateEntry {
 const TemplateEntry *template_table(int *n);
 
 }  // namespace fm
+
+#include "split.cuh"

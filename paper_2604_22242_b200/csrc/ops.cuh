@@ -16,6 +16,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 
 namespace fm {
 
@@ -297,6 +298,19 @@ __device__ __forceinline__ float d_to_bf(double a) {
 }
 __device__ __forceinline__ float bf16_bits_to_f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 __device__ __forceinline__ uint16_t f_to_bf16_bits(float a) { return (uint16_t)(__float_as_uint(rnd_bf_f(a)) >> 16); }
+
+// f32 -> three bf16 planes with x = hi + mid + lo + O(2^-24 |x|): each
+// residual is exact in f32 (Sterbenz), each plane the round-to-nearest bf16
+// of the residual (the f32 GEMM's operand planes, gemm_tc.cu).
+__device__ __forceinline__ void split3(float x, uint16_t &h, uint16_t &m, uint16_t &l) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+  const float r1 = __fsub_rn(x, __bfloat162float(hi));
+  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+  const float r2 = __fsub_rn(r1, __bfloat162float(mid));
+  h = __bfloat16_as_ushort(hi);
+  m = __bfloat16_as_ushort(mid);
+  l = __bfloat16_as_ushort(__float2bfloat16_rn(r2));
+}
 
 // ---- pow: left-associated repeated product (codegen.py:211-216) ------------------
 __device__ __forceinline__ float pow_f(float x, int k) {

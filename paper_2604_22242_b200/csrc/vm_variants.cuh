@@ -20,7 +20,9 @@ using Vm64d = Vm<true, 8, 4, 4>;
   extern template int run_copy<E>(const fm_program &, void *, int64_t, int64_t, cudaStream_t);    \
   extern template int run_accu<E>(const fm_program &, void *, int64_t, int64_t, int, cudaStream_t); \
   extern template int run_reduce_dim<E>(const fm_program &, int, int64_t, int64_t, const ReduceOuts &, \
-                                        cudaStream_t);
+                                        cudaStream_t);                                                  \
+  extern template int run_split<E>(const fm_program &, uint16_t *, int64_t, int64_t, int64_t, int64_t,  \
+                                   cudaStream_t);
 #ifndef FM_VM_VARIANT
 FM_VM_DECLARE(Vm32s)
 FM_VM_DECLARE(Vm32d)

@@ -119,6 +119,12 @@ class GemmStep:
     c_id: int | None = None
     alpha2: float = 1.0
     beta: float = 0.0
+    # prologue: an operand that is a MatMul-free elementwise expression is
+    # not materialised (the reference's plan.py:125-151 temp); its fused
+    # program runs inside the GEMM's operand pass (fm_gemm_prologue).  The
+    # step's a_id / b_id is then None and a_shape / b_shape the expression's.
+    a_expr: "FusedKernelStep | None" = None
+    b_expr: "FusedKernelStep | None" = None
 
     @property
     def m(self) -> int:
@@ -195,9 +201,11 @@ class _Planner:
         self.steps.append(FusedKernelStep.create(node, COPY, t.temp_id))
         return Leaf(t.temp_id, node.etype, node.shape)
 
-    def gemm_operand(self, node: ExprNode) -> tuple[Leaf, bool, float]:
+    def gemm_operand(self, node: ExprNode) -> tuple[ExprNode, bool, float]:
         """Peel scalar pre-multiplies and transposes off a product operand;
-        what remains is a dense leaf (used in place) or gets materialised."""
+        what remains is a dense leaf (used in place), a fused elementwise
+        expression (the GEMM's prologue, f32 / f64 operands), or gets
+        materialised."""
         alpha, trans = 1.0, False
         while True:
             if isinstance(node, UnaryElem) and node.kind is UnaryKind.scalar_pre_mul:
@@ -208,6 +216,9 @@ class _Planner:
                 node = node.child
             else:
                 break
+        node = self.fused(node)
+        if isinstance(node, Leaf) or node.etype in (ElemType.f32, ElemType.f64):
+            return node, trans, alpha
         return self.materialize(node), trans, alpha
 
     def gemm(self, node: MatMul, out_id: int | None = None) -> GemmStep:
@@ -215,8 +226,11 @@ class _Planner:
         b, tb, sb = self.gemm_operand(node.right)
         if out_id is None:
             out_id = self.temp(node.shape, node.etype).temp_id
-        step = GemmStep(a.mat_id, b.mat_id, out_id, a.shape, b.shape, ta, tb, sa * sb,
-                        a.etype, node.etype, node.shape)
+        a_expr = None if isinstance(a, Leaf) else FusedKernelStep.create(a, COPY, out_id)
+        b_expr = None if isinstance(b, Leaf) else FusedKernelStep.create(b, COPY, out_id)
+        step = GemmStep(a.mat_id if a_expr is None else None, b.mat_id if b_expr is None else None,
+                        out_id, a.shape, b.shape, ta, tb, sa * sb, a.etype, node.etype, node.shape,
+                        a_expr=a_expr, b_expr=b_expr)
         self.steps.append(step)
         return step
 
@@ -292,9 +306,19 @@ def _size(node: ExprNode) -> int:
     return sum(1 for _ in walk(node))
 
 
+# Leaf reads per launch the planner aims for: the widest ahead-of-time
+# template (aot_registry: the add-N chains up to 32 inputs).  A 33..40-leaf
+# program still lowers, but only onto the register VM, which streams many-leaf
+# chains at a third of the template rate (r02 suite: add48N 1.86 TB/s as a
+# 40-leaf VM launch + add9N, vs add32N 5.97); cutting at 32 costs one temp
+# write + read per 32 leaves (~6 % traffic) and keeps every piece on a template.
+PLAN_SLOTS = 32
+
+
 def _fits(node: ExprNode) -> bool:
-    """Does `node` lower within the fused-program limits?  Cheap bound first
-    (every node emits at most two instructions), the real lowering otherwise."""
+    """Does `node` lower within the fused-program limits (and the planner's
+    PLAN_SLOTS leaf budget)?  Cheap bound first (every node emits at most two
+    instructions), the real lowering otherwise."""
     n = leaves = scalars = 0
     for x in walk(node):
         n += 1
@@ -302,7 +326,9 @@ def _fits(node: ExprNode) -> bool:
             leaves += 1
         elif isinstance(x, UnaryElem) and x.kind in SCALAR_KINDS:
             scalars += 1
-    if 2 * n <= lw.MAX_INSTR and leaves <= lw.MAX_SLOTS and scalars <= lw.MAX_SCALARS:
+    if leaves > PLAN_SLOTS:
+        return False
+    if 2 * n <= lw.MAX_INSTR and scalars <= lw.MAX_SCALARS:
         return True
     try:
         lw.lower(node)

@@ -132,10 +132,28 @@ class SimBackend(Backend):
             return
         self.bufs[out.id][: v.size] = to_storage(v.ravel(order="F"), out.etype)
 
+    def bind(self, kernel, args):
+        return kernel, list(args)
+
+    def _operand(self, prog, rows, cols, etype):
+        # a prologue program: materialise it (the reference's temp) into a scratch buffer
+        kernel, args = prog
+        t = self.alloc(etype, rows * cols)
+        args[0] = t
+        self.launch(kernel, args, (rows, cols))
+        v = self._arr(t, rows, cols)
+        self.free(t)
+        return v
+
     def gemm(self, out, a, b, m, n, k, trans_a=False, trans_b=False, alpha=1.0, lda=None,
-             ldb=None, precision=0, c_in=None, alpha2=1.0, beta=0.0):
-        A = self._arr(a, k, m).T if trans_a else self._arr(a, m, k)
-        B = self._arr(b, n, k).T if trans_b else self._arr(b, k, n)
+             ldb=None, precision=0, c_in=None, alpha2=1.0, beta=0.0, a_prog=None, b_prog=None,
+             in_etype=None):
+        ar, ac = (k, m) if trans_a else (m, k)
+        br, bc = (n, k) if trans_b else (k, n)
+        A = self._operand(a_prog, ar, ac, in_etype) if a_prog is not None else self._arr(a, ar, ac)
+        B = self._operand(b_prog, br, bc, in_etype) if b_prog is not None else self._arr(b, br, bc)
+        A = A.T if trans_a else A
+        B = B.T if trans_b else B
         C = alpha * (A.astype(np.float64) @ B.astype(np.float64))
         C = C.astype(out.etype.dtype)
         if c_in is not None:

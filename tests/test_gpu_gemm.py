@@ -227,3 +227,74 @@ def test_accu_of_transposed_and_view_expressions(gpu_ctx):
     got = fm.accu(X.submat(5, 7, 300, 200) - Y.submat(1, 2, 300, 200))
     want = orc.accu(x[5:305, 7:207] - y[1:301, 2:202], orc.ElemType.f64)
     assert abs(got - want) <= 1e-12 * max(1.0, abs(want))
+
+
+# ---- operand prologues (csrc/split.cuh, fm_gemm_prologue): an elementwise
+# operand is evaluated inside the GEMM's operand pass, not materialised.  The
+# result must be bit-identical to the reference's plan -- the operand copied
+# into a temp, then the product (plan.py:125-151) -- on every path.
+
+def _two_step(ctx, operand_expr, shape, etype, product):
+    T = fm.Mat(*shape, etype, ctx)
+    T.assign(operand_expr)
+    return product(T)
+
+
+@pytest.mark.parametrize("etype,mnk", [("f32", (640, 768, 576)),    # tensor path (split planes)
+                                       ("f32", (96, 80, 72)),       # exact path (materialised in C)
+                                       ("f64", (96, 80, 72))])
+def test_gemm_prologue_bit_identical_to_materialised(gpu_ctx, etype, mnk):
+    m, n, k = mnk
+    X = fm.randu(m, k, 1, etype, gpu_ctx)
+    Y = fm.randu(m, k, 2, etype, gpu_ctx)
+    Z = fm.randu(k, n, 3, etype, gpu_ctx)
+    out = fm.Mat(m, n, etype, gpu_ctx)
+    gpu_ctx.reset_counters()
+    out.assign((X + 2 * Y) @ Z)
+    assert gpu_ctx.launches == 1                  # no operand temp launch
+    want = _two_step(gpu_ctx, X + 2 * Y, (m, k), etype, lambda T: T @ Z)
+    ref = fm.Mat(m, n, etype, gpu_ctx)
+    ref.assign(want)
+    assert np.array_equal(out.to_numpy(), ref.to_numpy())
+    x, y, z = X.to_numpy(), Y.to_numpy(), Z.to_numpy()
+    t = x + x.dtype.type(2) * y
+    _check(out.to_numpy(), t, z, 1.0)
+
+
+def test_gemm_prologue_both_operands_transposed_and_views(gpu_ctx):
+    m, n, k = 512, 640, 1024                      # tensor path
+    A = fm.randu(k, m, 11, "f32", gpu_ctx)        # used as A.t()
+    B = fm.randu(k, m, 12, "f32", gpu_ctx)
+    W = fm.randu(n + 8, k + 4, 13, "f32", gpu_ctx)
+    out = fm.Mat(m, n, "f32", gpu_ctx)
+    rhs = (W.submat(8, 4, n, k) - 0.5).t()
+    out.assign(3.0 * ((A % B).t() @ rhs))
+    a, b, w = A.to_numpy(), B.to_numpy(), W.to_numpy()
+    lhs_v = (a * b).T
+    rhs_v = (w[8:8 + n, 4:4 + k] + np.float32(-0.5)).T
+    ref_l = fm.Mat(k, m, "f32", gpu_ctx)
+    ref_l.assign(A % B)
+    ref_r = fm.Mat(n, k, "f32", gpu_ctx)
+    ref_r.assign(W.submat(8, 4, n, k) - 0.5)
+    ref = fm.Mat(m, n, "f32", gpu_ctx)
+    ref.assign(3.0 * (ref_l.t() @ ref_r.t()))
+    assert np.array_equal(out.to_numpy(), ref.to_numpy())
+    _check(out.to_numpy(), lhs_v, rhs_v, 3.0)
+
+
+def test_gemm_prologue_with_epilogue_and_graph(gpu_ctx):
+    m, n, k = 512, 512, 1024
+    X = fm.randu(m, k, 21, "f32", gpu_ctx)
+    Z = fm.randu(k, n, 22, "f32", gpu_ctx)
+    C = fm.randu(m, n, 23, "f32", gpu_ctx)
+    out = fm.Mat(m, n, "f32", gpu_ctx)
+    g = fm.capture(lambda: out.assign(2 * (fm.abs(X - 0.5) @ Z) + C), gpu_ctx)
+    g.replay()
+    g.replay()
+    gpu_ctx.sync()
+    T = fm.Mat(m, k, "f32", gpu_ctx)
+    T.assign(fm.abs(X - 0.5))
+    ref = fm.Mat(m, n, "f32", gpu_ctx)
+    ref.assign(2 * (T @ Z) + C)
+    assert np.array_equal(out.to_numpy(), ref.to_numpy())
+    g.close()

@@ -80,12 +80,27 @@ def test_c5_gemm_folds_scalar_and_transpose_into_one_launch():
     assert (g.m, g.n, g.k) == (64, 48, 32) and g.out_id == OUT
 
 
-def test_gemm_operand_expression_materialised_once():
+def test_gemm_operand_expression_is_a_prologue():
+    """An elementwise operand is not materialised (the reference's temp,
+    plan.py:125-151): it becomes the GEMM's prologue program over its stored
+    shape, the transpose still folded into the product."""
     node = ast.matmul(ast.transpose(ast.plus(L(0, 4, 8), L(1, 4, 8))), L(2, 4, 2))
     pl = P.plan(OUT, node)
-    assert len(pl.fused_steps) == 1 and len(pl.gemm_steps) == 1
-    assert pl.fused_steps[0].out_shape == MatShape(4, 8)      # no transpose copy
-    assert pl.gemm_steps[0].trans_a
+    assert len(pl.fused_steps) == 0 and len(pl.gemm_steps) == 1 and not pl.temps
+    g = pl.gemm_steps[0]
+    assert g.trans_a and g.a_id is None and g.b_id == 2
+    assert g.a_expr.out_shape == MatShape(4, 8)              # no transpose copy
+    assert sorted(s.mat_id for s in g.a_expr.inputs) == [0, 1]
+
+
+def test_gemm_prologue_keeps_inner_barriers():
+    """A reduction / product inside the operand is still its own launch; the
+    rest of the operand rides in the GEMM."""
+    inner = ast.matmul(L(0, 4, 3), L(1, 3, 8))
+    node = ast.matmul(ast.plus(inner, L(2, 4, 8)), L(3, 8, 2))
+    pl = P.plan(OUT, node)
+    assert len(pl.gemm_steps) == 2 and len(pl.fused_steps) == 0
+    assert pl.gemm_steps[1].a_expr is not None
 
 
 def test_chain_three_gemms_left_to_right():
@@ -167,18 +182,20 @@ def _addn(n, t=F32):
     return e
 
 
-@pytest.mark.parametrize("n", [40, 41, 48, 64, 200])
+@pytest.mark.parametrize("n", [32, 33, 40, 41, 48, 64, 200])
 def test_planner_splits_trees_past_the_program_limits(n):
     """add-N for any N (reference bench.py:307-326 sweeps it unbounded): the
-    planner cuts the tree into launches that each lower within the limits,
-    materialising sub-sums into temps; every input is read exactly once."""
+    planner cuts the tree into launches of at most PLAN_SLOTS (32, the widest
+    AOT template) leaf reads, materialising sub-sums into temps; every input
+    is read exactly once."""
     pl = P.plan(OUT, _addn(n))
     steps = pl.fused_steps
-    assert len(steps) == -(-(n - 1) // (lower.MAX_SLOTS - 1)) if n > lower.MAX_SLOTS else len(steps) == 1
+    k = P.PLAN_SLOTS
+    assert len(steps) == -(-(n - 1) // (k - 1)) if n > k else len(steps) == 1
     reads = []
     for st in steps:
         prog = lower.lower(st.expr)                      # each launch lowers
-        assert len(prog.slots) <= lower.MAX_SLOTS
+        assert len(prog.slots) <= k <= lower.MAX_SLOTS
         reads += [s.mat_id for s in st.inputs if s.mat_id >= 0]
     assert sorted(reads) == list(range(n))
     assert steps[-1].out_id == OUT
