@@ -817,12 +817,14 @@ class C5(Config):
 
 
 class C5F32(C5):
-    """f32 operands: each split into three bf16 planes, the six significant
-    plane products accumulated by the same tcgen05 kernel (two split launches
-    + the GEMM).  TFLOP/s counts the f32 product's 2*N^3."""
+    """f32 operands: each scaled by a power of two from its max |x| and split
+    into two fp16 planes (hi + lo, 22 significant bits), the three
+    significant plane products accumulated by the same tcgen05 kernel (two
+    max-abs + two split launches + the GEMM).  TFLOP/s counts the f32
+    product's 2*N^3."""
     name = "c5f32"
     etype = "f32"
-    dtype = "f32 operands (3 bf16 planes each, f32 accumulate, f32 out)"
+    dtype = "f32 operands (2 scaled fp16 planes each, 3 products, f32 accumulate, f32 out)"
     metric = "fused 2*X*Y.t() GEMM TFLOP/s (BASELINE.json configs[4], f32 operands)"
 
 

@@ -36,7 +36,9 @@ int sm_count();
 // copy into a buffer (operands of the exact GEMM path)
 int validate_program(const fm_program *P);
 int launch_split_program(const fm_program &P, uint16_t *planes, int64_t n_rows, int64_t n_cols, int64_t ld_out,
-                         int64_t plane_off, cudaStream_t s);
+                         int64_t plane_off, const unsigned *amax, cudaStream_t s);
+int launch_amax_program(const fm_program &P, int64_t n_rows, int64_t n_cols, unsigned *amax, cudaStream_t s,
+                        bool *handled);
 int launch_copy_program(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s);
 
 // Programmatic dependent launch: kernels launched through launch_pdl may

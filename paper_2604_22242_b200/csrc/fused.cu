@@ -6,6 +6,7 @@
 // kernel id from fm_kernel_lookup selects an ahead-of-time template kernel;
 // id -1 runs the same program on the VM.  Either way one launch per fused
 // step.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -58,14 +59,55 @@ template <class E> struct DimF {
 };
 
 template <class E> struct SplitF {
-  static int run(const fm_program &P, uint16_t *o, int64_t r, int64_t c, int64_t ld, int64_t po, cudaStream_t s) {
-    return run_split<E>(P, o, r, c, ld, po, s);
+  static int run(const fm_program &P, uint16_t *o, int64_t r, int64_t c, int64_t ld, int64_t po, const unsigned *am,
+                 cudaStream_t s) {
+    return run_split<E>(P, o, r, c, ld, po, am, s);
   }
 };
 
 int launch_split_program(const fm_program &P, uint16_t *planes, int64_t n_rows, int64_t n_cols, int64_t ld_out,
-                         int64_t plane_off, cudaStream_t s) {
-  return vm_dispatch<SplitF>(P, planes, n_rows, n_cols, ld_out, plane_off, s);
+                         int64_t plane_off, const unsigned *amax, cudaStream_t s) {
+  return vm_dispatch<SplitF>(P, planes, n_rows, n_cols, ld_out, plane_off, amax, s);
+}
+
+// max |EXPR| over the domain as f32 bits, atomically max-ed into *amax:
+// the program with one ABS appended, column maxima (dim-0 MAX reduction,
+// NaN propagates), then the maximum of those.  handled = false when the
+// program has no room for the extra instruction.
+__global__ void k_amax_vec(const float *v, int64_t n, unsigned *amax) {
+  unsigned m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(v[i]) & 0x7fffffffu);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(amax, m);
+}
+
+int launch_amax_program(const fm_program &P0, int64_t n_rows, int64_t n_cols, unsigned *amax, cudaStream_t s,
+                        bool *handled) {
+  *handled = false;
+  if (P0.n_instr >= FM_MAX_INSTR || P0.result_etype != FM_F32 || n_rows == 0 || n_cols == 0) return 0;
+  fm_program P = P0;
+  P.code[P.n_instr].key = (uint16_t)(FM_OP_ABS_F << 3);
+  P.code[P.n_instr].arg = 0;
+  ++P.n_instr;
+  float *colmax = nullptr;
+  FM_CHECK(cudaMallocAsync((void **)&colmax, (size_t)n_cols * sizeof(float), s));
+  ReduceOuts R;
+  R.n = 1;
+  R.o[0].kind = FM_RED_MAX;
+  R.o[0].etype = FM_F32;
+  R.o[0].out = colmax;
+  int st = vm_dispatch<DimF>(P, 0, n_rows, n_cols, R, s);
+  if (!st) {
+    k_amax_vec<<<(unsigned)std::min<int64_t>((n_cols + 255) / 256, 148), 256, 0, s>>>(colmax, n_cols, amax);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) st = fail("operand max |x| kernel", e);
+    else count_launch();
+  }
+  cudaFreeAsync(colmax, s);
+  if (!st) *handled = true;
+  return st;
 }
 int launch_copy_program(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cudaStream_t s) {
   return vm_dispatch<CopyF>(P, out, n_rows, n_cols, s);

@@ -23,6 +23,7 @@
 // tile i overlap the MMAs of tile i+1.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -51,6 +52,10 @@ constexpr int kThreadsTc = (2 + kEpiWarps) * 32;
 // (a single 8192-deep accumulation measured 3.1e-5, bound 6.1e-5).  Measured
 // at C5 (8192^3 bf16): KC=8 1340 TF/s, 16 1436, 32 1452, unchunked 1465.
 constexpr int KC = 16;
+// fp16-plane scheme: drain every 8 virtual k-blocks (C5 f32: max rel err
+// 6.0e-6 at 16, 2.9e-6 at 8, 1.5e-6 at 4 from the accumulator's per-step
+// truncation; 360 / 352 / 335 TF/s)
+constexpr int KC_F16 = 8;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int GROUP_M = 8;                          // tile rasterisation: 8 M-blocks share B in L2
 
@@ -145,10 +150,10 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-// instruction descriptor, kind::f16: bf16 x bf16 -> f32, M = BM, N = BN
-__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
-  return (1u << 4)                       // D format f32
-         | (1u << 7) | (1u << 10)        // A, B format bf16
+// instruction descriptor, kind::f16: bf16 x bf16 (or fp16 x fp16) -> f32, M = BM, N = BN
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, bool f16 = false) {
+  return (1u << 4)                                      // D format f32
+         | (f16 ? 0u : ((1u << 7) | (1u << 10)))        // A, B format: bf16 = 1, fp16 = 0
          | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16)
          | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
@@ -160,7 +165,7 @@ struct Params {
   float alpha;
   int a_mn, b_mn;   // operand major-ness (1 = MN-contiguous)
   int nkb;          // k-blocks per product
-  int nprod;        // 1 (bf16 operands) or 6 (f32 operands split into 3 bf16 planes)
+  int nprod;        // 1 (bf16 operands), 3 (f32: 2 fp16 planes) or 6 (f32: 3 bf16 planes)
   int kplane;       // K offset between stacked planes (elements, multiple of BK)
   uint32_t pa, pb;  // plane of A / B used by product p: bits [3p, 3p+3)
   int kc;           // virtual k-blocks per TMEM drain (KC unless overridden)
@@ -168,7 +173,16 @@ struct Params {
   int64_t ldcin;
   float alpha2, beta;
   int group_m;      // M-blocks per rasterisation group (L2 reuse of B)
+  int f16;          // operands are fp16 planes (f32 inputs, two scaled planes)
+  const unsigned *amax;  // [2] max |A|, max |B| bits (fp16 planes: power-of-two scales), or nullptr
 };
+
+// epilogue scale: alpha * 2^-(ea + eb), exact (a power of two)
+__device__ __forceinline__ float epilogue_alpha(const Params &p) {
+  if (!p.amax) return p.alpha;
+  const int e = f16_scale_exp(p.amax[0]) + f16_scale_exp(p.amax[1]);
+  return p.alpha * ldexpf(1.0f, -e);
+}
 
 __device__ __forceinline__ void tile_coords(int t, int ntm, int ntn, int &mb, int &nb, int group_m = GROUP_M) {
   const int per_group = group_m * ntn;
@@ -255,7 +269,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
   } else if (warp == 1) {
     // ===== MMA issuer: one TMEM accumulator per chunk of KC virtual k-blocks =====
-    const uint32_t idesc = make_idesc(p.a_mn != 0, p.b_mn != 0);
+    const uint32_t idesc = make_idesc(p.a_mn != 0, p.b_mn != 0, p.f16 != 0);
     // per UMMA_K step: K-major advances 32 B inside the swizzled row;
     // MN-major advances two 1024-B k-groups.
     const uint32_t a_step = p.a_mn ? 2048u : 32u, b_step = p.b_mn ? 2048u : 32u;
@@ -293,6 +307,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
   } else {
     // ===== epilogue: drain each chunk into f32 register sums, then alpha * sum -> column-major stores =====
+    const float ealpha = epilogue_alpha(p);
     const int q = warp & 3;                    // TMEM lane quarter this warp may access
     const int h = (warp - 2) >> 2;             // column half (128 columns)
     uint32_t gc = 0;
@@ -329,14 +344,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
           for (int j = 0; j < BN / 2; ++j)
             if (col0 + j < p.n) {
-              const float t = __fmul_rn(p.alpha, sum[j]);
+              const float t = __fmul_rn(ealpha, sum[j]);
               cp[(int64_t)(col0 + j) * p.ldc] =
                   __fadd_rn(__fmul_rn(p.alpha2, t), __fmul_rn(p.beta, ci[(int64_t)(col0 + j) * p.ldcin]));
             }
         } else {
 #pragma unroll
           for (int j = 0; j < BN / 2; ++j)
-            if (col0 + j < p.n) cp[(int64_t)(col0 + j) * p.ldc] = p.alpha * sum[j];
+            if (col0 + j < p.n) cp[(int64_t)(col0 + j) * p.ldc] = __fmul_rn(ealpha, sum[j]);
         }
       }
     }
@@ -407,9 +422,9 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
       "h"((uint16_t)3)
       : "memory");
 }
-__host__ __device__ constexpr uint32_t make_idesc_pair(bool a_mn, bool b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(BM2 >> 4) << 24);
+__host__ __device__ constexpr uint32_t make_idesc_pair(bool a_mn, bool b_mn, bool f16 = false) {
+  return (1u << 4) | (f16 ? 0u : ((1u << 7) | (1u << 10))) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(BM2 >> 4) << 24);
 }
 }  // namespace pair
 
@@ -496,7 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTc, 1)
   } else if (warp == 1) {
     // ===== MMA issuer: leader only
     if (leader) {
-      const uint32_t idesc = make_idesc_pair(p.a_mn != 0, p.b_mn != 0);
+      const uint32_t idesc = make_idesc_pair(p.a_mn != 0, p.b_mn != 0, p.f16 != 0);
       const uint32_t a_step = p.a_mn ? 2048u : 32u, b_step = p.b_mn ? 2048u : 32u;
       const uint32_t a_lbo = p.a_mn ? 64u * BK * 2 : 16u, b_lbo = p.b_mn ? 64u * BK * 2 : 16u;
       int stage = 0;
@@ -533,6 +548,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTc, 1)
     }
   } else {
     // ===== epilogue (both CTAs): this CTA's 128 accumulator rows
+    const float ealpha = epilogue_alpha(p);
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;
     uint32_t gc = 0;
@@ -569,14 +585,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
           for (int j = 0; j < BN2 / 2; ++j)
             if (col0 + j < p.n) {
-              const float tt = __fmul_rn(p.alpha, sum[j]);
+              const float tt = __fmul_rn(ealpha, sum[j]);
               cp[(int64_t)(col0 + j) * p.ldc] =
                   __fadd_rn(__fmul_rn(p.alpha2, tt), __fmul_rn(p.beta, ci[(int64_t)(col0 + j) * p.ldcin]));
             }
         } else {
 #pragma unroll
           for (int j = 0; j < BN2 / 2; ++j)
-            if (col0 + j < p.n) cp[(int64_t)(col0 + j) * p.ldc] = p.alpha * sum[j];
+            if (col0 + j < p.n) cp[(int64_t)(col0 + j) * p.ldc] = __fmul_rn(ealpha, sum[j]);
         }
       }
     }
@@ -627,6 +643,51 @@ __global__ void k_split3(const float *__restrict__ in, int64_t rows, int64_t col
   }
 }
 
+// max |x| of a column-major operand as f32 bits (non-negative floats order
+// like their bit patterns; NaN bits sort above +inf) -> atomicMax into *out.
+__global__ void k_amax(const float *__restrict__ in, int64_t rows, int64_t cols, int64_t ld, unsigned *out) {
+  unsigned m = 0;
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    const float *src = in + j * ld;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+      m = max(m, __float_as_uint(src[i]) & 0x7fffffffu);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void k_split2h(const float *__restrict__ in, int64_t rows, int64_t cols, int64_t ld_in,
+                          uint16_t *__restrict__ out, int64_t ld_out, int64_t plane_off, const unsigned *amax) {
+  const float sc = ldexpf(1.0f, f16_scale_exp(*amax));
+  const bool vec = ((ld_in & 3) == 0) && ((ld_out & 3) == 0) && ((plane_off & 3) == 0) &&
+                   ((((uintptr_t)in) & 15) == 0) && ((((uintptr_t)out) & 7) == 0);
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    const float *src = in + j * ld_in;
+    uint16_t *dst = out + j * ld_out;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x * 4) {
+      if (vec && i + 4 <= rows) {
+        const float4 x = *(const float4 *)(src + i);
+        ushort4 h, l;
+        split2h(x.x, sc, h.x, l.x);
+        split2h(x.y, sc, h.y, l.y);
+        split2h(x.z, sc, h.z, l.z);
+        split2h(x.w, sc, h.w, l.w);
+        *(ushort4 *)(dst + i) = h;
+        *(ushort4 *)(dst + i + plane_off) = l;
+      } else {
+        for (int64_t ii = i; ii < i + 4 && ii < rows; ++ii) {
+          uint16_t h, l;
+          split2h(src[ii], sc, h, l);
+          dst[ii] = h;
+          dst[ii + plane_off] = l;
+        }
+      }
+    }
+  }
+}
+
 // ---- host side -----------------------------------------------------------------------
 // cuTensorMapEncodeTiled comes from the driver through the runtime's entry-point
 // query, so libfmb200.so has no link-time dependency on libcuda (it still loads
@@ -666,10 +727,13 @@ static int encode_map(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_
 
 }  // namespace tc
 
-// Tensor-core path: bf16 operands directly; f32 operands split into three
-// bf16 planes each (k_split3) and multiplied as the six significant plane
-// products hi*hi, hi*mid, mid*hi, hi*lo, mid*mid, lo*hi in one kernel launch
-// (dropped terms are O(2^-24) relative).  Shapes TMA cannot describe report
+// Tensor-core path: bf16 operands directly; f32 operands scaled by a power
+// of two from their max |x| (k_amax) and split into two fp16 planes each
+// (k_split2h / the prologue's fused split), multiplied as the three
+// significant plane products lo*hi, hi*lo, hi*hi in one kernel launch
+// (dropped lo*lo and plane rounding: O(2^-21) relative).  The older
+// three-bf16-plane, six-product scheme (k_split3) remains for a prologue
+// program with no room for its max pass.  Shapes TMA cannot describe report
 // handled = false and run on the exact kernel.
 bool gemm_tensor_supported(const fm_gemm_args &g) {
   if (g.out_etype != FM_F32) return false;
@@ -690,28 +754,35 @@ struct Planes {
   uint16_t *buf = nullptr;
   uint64_t inner = 0, outer = 0, ld = 0;
 };
+// nplanes = 3: bf16 hi/mid/lo; nplanes = 2: scaled fp16 hi/lo (amax = max |src| bits on the device)
 int split_operand(const float *src, int64_t rows, int64_t cols, int64_t ld_in, bool k_is_cols, int64_t kplane,
-                  Planes *pl, cudaStream_t s, const fm_program *prog) {
+                  Planes *pl, cudaStream_t s, const fm_program *prog, int nplanes = 3,
+                  const unsigned *amax = nullptr) {
   int64_t ld_out, plane_off, bytes;
   if (k_is_cols) {   // MN-major operand: planes appended along the column (K) dimension
     ld_out = round_up(rows, 8);
     plane_off = kplane * ld_out;
-    bytes = 3 * plane_off * 2;
-    pl->inner = (uint64_t)rows; pl->outer = (uint64_t)(3 * kplane);
+    bytes = nplanes * plane_off * 2;
+    pl->inner = (uint64_t)rows; pl->outer = (uint64_t)(nplanes * kplane);
   } else {           // K-major operand: planes stacked along the row (K) dimension
-    ld_out = 3 * kplane;
+    ld_out = nplanes * kplane;
     plane_off = kplane;
     bytes = ld_out * cols * 2;
-    pl->inner = (uint64_t)(3 * kplane); pl->outer = (uint64_t)cols;
+    pl->inner = (uint64_t)(nplanes * kplane); pl->outer = (uint64_t)cols;
   }
   pl->ld = (uint64_t)ld_out;
   FM_CHECK(cudaMallocAsync((void **)&pl->buf, (size_t)bytes, s));
   const int64_t kdim = k_is_cols ? cols : rows;
   if (kdim != kplane) FM_CHECK(cudaMemsetAsync(pl->buf, 0, (size_t)bytes, s));   // zero K padding
   if (prog)   // operand prologue: the operand's expression evaluated into the planes (split.cuh)
-    return launch_split_program(*prog, pl->buf, rows, cols, ld_out, plane_off, s);
+    return launch_split_program(*prog, pl->buf, rows, cols, ld_out, plane_off, nplanes == 2 ? amax : nullptr, s);
   const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 1023) / 1024, 64));
   const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cols, 65535));
+  if (nplanes == 2) {
+    tc::k_split2h<<<dim3(gx, gy), 256, 0, s>>>(src, rows, cols, ld_in, pl->buf, ld_out, plane_off, amax);
+    FM_CHECK_LAUNCH("f32 -> scaled fp16 plane split kernel");
+    return 0;
+  }
   tc::k_split3<<<dim3(gx, gy), 256, 0, s>>>(src, rows, cols, ld_in, pl->buf, ld_out, plane_off);
   FM_CHECK_LAUNCH("f32 -> bf16 plane split kernel");
   return 0;
@@ -758,20 +829,64 @@ int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled, const fm_p
   CUtensorMap ma, mb;
   int st;
   Planes pa, pb;
+  p.f16 = 0;
+  p.amax = nullptr;
+  unsigned *amax = nullptr;
   if (g.in_etype == FM_F32) {
     const int64_t kplane = round_up(g.k, BK);
-    p.nprod = 6;
     p.kplane = (int)kplane;
-    // products, smallest first: (0,2) (1,1) (2,0) (0,1) (1,0) (0,0)
-    const uint32_t A[6] = {0, 1, 2, 0, 1, 0}, B[6] = {2, 1, 0, 1, 0, 0};
-    p.pa = p.pb = 0;
-    for (int i = 0; i < 6; ++i) { p.pa |= A[i] << (3 * i); p.pb |= B[i] << (3 * i); }
-    st = p.a_mn ? split_operand((const float *)g.a, g.m, g.k, g.lda, true, kplane, &pa, s, a_prog)
-                : split_operand((const float *)g.a, g.k, g.m, g.lda, false, kplane, &pa, s, a_prog);
-    if (st) return st;
-    st = p.b_mn ? split_operand((const float *)g.b, g.n, g.k, g.ldb, true, kplane, &pb, s, b_prog)
-                : split_operand((const float *)g.b, g.k, g.n, g.ldb, false, kplane, &pb, s, b_prog);
-    if (st) { cudaFreeAsync(pa.buf, s); return st; }
+    // f32 operands: two fp16 planes each, scaled by a power of two from the
+    // operand's max |x| (one short device pass: a max-abs kernel, or for an
+    // operand prologue a MAX reduction of |expression|), and the three
+    // significant products hi*lo, lo*hi, hi*hi -- half the tensor work of
+    // the six-product bf16 scheme at ~2^-21 relative per term.  The bf16
+    // scheme remains for a prologue program with no room for the max pass.
+    const int64_t ar = p.a_mn ? g.m : g.k, ac = p.a_mn ? g.k : g.m;
+    const int64_t br = p.b_mn ? g.n : g.k, bc = p.b_mn ? g.k : g.n;
+    bool f16 = true;
+    for (const fm_program *P : {a_prog, b_prog})
+      if (P && P->n_instr >= FM_MAX_INSTR) f16 = false;
+    int nplanes = 3;
+    if (f16) {
+      nplanes = 2;
+      p.f16 = 1;
+      p.nprod = 3;
+      p.kc = std::min(p.kc, KC_F16);
+      const uint32_t A[3] = {0, 1, 0}, B[3] = {1, 0, 0};
+      p.pa = p.pb = 0;
+      for (int i = 0; i < 3; ++i) { p.pa |= A[i] << (3 * i); p.pb |= B[i] << (3 * i); }
+      FM_CHECK(cudaMallocAsync((void **)&amax, 2 * sizeof(unsigned), s));
+      FM_CHECK(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned), s));
+      const fm_program *progs[2] = {a_prog, b_prog};
+      const void *bufs[2] = {g.a, g.b};
+      const int64_t rows[2] = {ar, br}, cols[2] = {ac, bc}, lds[2] = {g.lda, g.ldb};
+      for (int o = 0; o < 2; ++o) {
+        if (progs[o]) {
+          bool ok = false;
+          if (int e = launch_amax_program(*progs[o], rows[o], cols[o], amax + o, s, &ok)) { cudaFreeAsync(amax, s); return e; }
+        } else {
+          tc::k_amax<<<dim3((unsigned)std::min<int64_t>((rows[o] + 255) / 256, 16),
+                            (unsigned)std::min<int64_t>(cols[o], 2048)), 256, 0, s>>>((const float *)bufs[o], rows[o],
+                                                                                     cols[o], lds[o], amax + o);
+          FM_CHECK_LAUNCH("operand max |x| kernel");
+        }
+      }
+      p.amax = amax;
+    } else {
+      p.nprod = 6;
+      // products, smallest first: (0,2) (1,1) (2,0) (0,1) (1,0) (0,0)
+      const uint32_t A[6] = {0, 1, 2, 0, 1, 0}, B[6] = {2, 1, 0, 1, 0, 0};
+      p.pa = p.pb = 0;
+      for (int i = 0; i < 6; ++i) { p.pa |= A[i] << (3 * i); p.pb |= B[i] << (3 * i); }
+    }
+    st = p.a_mn ? split_operand((const float *)g.a, g.m, g.k, g.lda, true, kplane, &pa, s, a_prog, nplanes, amax)
+                : split_operand((const float *)g.a, g.k, g.m, g.lda, false, kplane, &pa, s, a_prog, nplanes, amax);
+    if (st) { if (amax) cudaFreeAsync(amax, s); return st; }
+    st = p.b_mn ? split_operand((const float *)g.b, g.n, g.k, g.ldb, true, kplane, &pb, s, b_prog, nplanes,
+                                amax ? amax + 1 : nullptr)
+                : split_operand((const float *)g.b, g.k, g.n, g.ldb, false, kplane, &pb, s, b_prog, nplanes,
+                                amax ? amax + 1 : nullptr);
+    if (st) { cudaFreeAsync(pa.buf, s); if (amax) cudaFreeAsync(amax, s); return st; }
     st = encode_map(&ma, pa.buf, pa.inner, pa.outer, pa.ld, p.a_mn ? 64 : BK, p.a_mn ? BK : BM);
     if (!st) st = encode_map(&mb, pb.buf, pb.inner, pb.outer, pb.ld, p.b_mn ? 64 : BK, p.b_mn ? BK : b_box_rows);
   } else {
@@ -803,6 +918,7 @@ int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled, const fm_p
     }
     if (pa.buf) cudaFreeAsync(pa.buf, s);
     if (pb.buf) cudaFreeAsync(pb.buf, s);
+    if (amax) cudaFreeAsync(amax, s);
     if (!st) *handled = true;
     return st;
   }
@@ -824,6 +940,7 @@ int gemm_tensor(const fm_gemm_args &g, cudaStream_t s, bool *handled, const fm_p
   }
   if (pa.buf) cudaFreeAsync(pa.buf, s);   // stream-ordered: released after the GEMM reads it
   if (pb.buf) cudaFreeAsync(pb.buf, s);
+  if (amax) cudaFreeAsync(amax, s);
   if (!st) *handled = true;
   return st;
 }

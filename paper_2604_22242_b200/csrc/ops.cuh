@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace fm {
 
@@ -310,6 +311,23 @@ __device__ __forceinline__ void split3(float x, uint16_t &h, uint16_t &m, uint16
   h = __bfloat16_as_ushort(hi);
   m = __bfloat16_as_ushort(mid);
   l = __bfloat16_as_ushort(__float2bfloat16_rn(r2));
+}
+
+// The f32 GEMM's fp16 operand planes (gemm_tc.cu): an operand is scaled by
+// 2^e with max|x| * 2^e in [2^14, 2^15) -- fp16 keeps 11 significant bits
+// over ~30 binades; the scale keeps the hi plane far from overflow and the lo
+// plane mostly normal -- then x * 2^e = hi + lo + O(2^-22 |x * 2^e|) with
+// hi = fp16(x * 2^e), lo = fp16(x * 2^e - hi) (the residual is exact in f32).
+__host__ __device__ inline int f16_scale_exp(unsigned amax_bits) {
+  const int be = (int)((amax_bits >> 23) & 0xff);
+  if (be == 0 || be == 0xff) return 0;   // zero / subnormal max, or a non-finite input: unscaled
+  return 14 - (be - 127);
+}
+__device__ __forceinline__ void split2h(float x, float sc, uint16_t &h, uint16_t &l) {
+  const float y = __fmul_rn(x, sc);
+  const __half hi = __float2half_rn(y);
+  h = __half_as_ushort(hi);
+  l = __half_as_ushort(__float2half_rn(__fsub_rn(y, __half2float(hi))));
 }
 
 // ---- pow: left-associated repeated product (codegen.py:211-216) ------------------

@@ -26,7 +26,8 @@ template int run_accu<VmT>(const fm_program &, void *, int64_t, int64_t, int, cu
 #elif FM_VM_SKELETON == 2
 template int run_reduce_dim<VmT>(const fm_program &, int, int64_t, int64_t, const ReduceOuts &, cudaStream_t);
 #else
-template int run_split<VmT>(const fm_program &, uint16_t *, int64_t, int64_t, int64_t, int64_t, cudaStream_t);
+template int run_split<VmT>(const fm_program &, uint16_t *, int64_t, int64_t, int64_t, int64_t, const unsigned *,
+                            cudaStream_t);
 #endif
 
 }  // namespace fm

@@ -22,7 +22,7 @@ using Vm64d = Vm<true, 8, 4, 4>;
   extern template int run_reduce_dim<E>(const fm_program &, int, int64_t, int64_t, const ReduceOuts &, \
                                         cudaStream_t);                                                  \
   extern template int run_split<E>(const fm_program &, uint16_t *, int64_t, int64_t, int64_t, int64_t,  \
-                                   cudaStream_t);
+                                   const unsigned *, cudaStream_t);
 #ifndef FM_VM_VARIANT
 FM_VM_DECLARE(Vm32s)
 FM_VM_DECLARE(Vm32d)

@@ -430,8 +430,9 @@ def test_capture_of_an_aliasing_assign_owns_its_buffers(ctx):
 
 @pytest.mark.parametrize("n_terms", [48, 64])
 def test_addn_past_the_program_limits(ctx, n_terms):
-    """add-N beyond one fused program (40 leaf reads): the planner splits it
-    into ceil((N-1)/39) launches through temps, still bit-exact."""
+    """add-N beyond the planner's 32-leaf budget (plan.PLAN_SLOTS, the widest
+    AOT template): split into ceil((N-1)/31) launches through temps, still
+    bit-exact."""
     mats = [fm.randu(129, 65, seed=100 + i, ctx=ctx) for i in range(n_terms)]
     e = mats[0] + mats[1]
     for m in mats[2:]:
@@ -439,7 +440,7 @@ def test_addn_past_the_program_limits(ctx, n_terms):
     z = fm.zeros(129, 65, ctx=ctx)
     ctx.reset_counters()
     z.assign(e)
-    assert ctx.launches == -(-(n_terms - 1) // 39)
+    assert ctx.launches == -(-(n_terms - 1) // 31)
     want = mats[0].to_numpy() + mats[1].to_numpy()
     for m in mats[2:]:
         want = want + m.to_numpy()

@@ -8,9 +8,10 @@ Bound (elementwise): |got - want| <= 1e-5 * sum_p |a_ip| |b_pj|.
   accumulator into round-to-nearest f32 register sums every 1024 of K, so
   the truncation error is <= 64 * 2^-23 = 7.6e-6 for any K (one 8192-deep
   TMEM accumulation measured 3.1e-5 before chunking).
-* f32 operands: each is split into three bf16 planes (x = hi + mid + lo +
-  O(2^-24 x)) and the six significant plane products are accumulated in the
-  same launch; the dropped terms are O(2^-24), so the same 1e-5 holds.
+* f32 operands: each is scaled by a power of two from its max |x| and split
+  into two fp16 planes (x 2^e = hi + lo + O(2^-22)); the three significant
+  plane products are accumulated in the same launch, drained every 512 of K;
+  the dropped terms are O(2^-21), so the same 1e-5 holds.
 """
 
 import numpy as np
