@@ -1,5 +1,7 @@
 """The BASELINE configs at their full bench sizes, checked through the
-oracle on sampled columns and through size-independent properties:
+oracle on EVERY element (C1, C3, C4: column blocks copied out with a fused
+subview copy and compared on the host) and through size-independent
+properties:
 
 * C2: dot / accu / norm of 1e8-element f32 and f64 vectors vs the exactly
   rounded f64 sum (rel 1e-12), accu(x % y) == dot(x, y) bit for bit (same
@@ -173,3 +175,63 @@ def test_row_stats_fast_path_nan_and_ties(ctx, etype):
         assert np.array_equal(got, want, equal_nan=True), (fn.__name__,)
     got = fm.sum(X, 1).eval().to_numpy()
     assert orc.compare(got, orc.reduce_dim(orc.ReduceKind.sum, 1, a, ety)) < 1e-12
+
+
+def _block(M, j0, w):
+    """Columns j0..j0+w-1 of a device matrix (one fused subview copy)."""
+    b = fm.Mat(M.n_rows, w, M.etype, M.ctx)
+    b.assign(M.submat(0, j0, M.n_rows, w))
+    return b.to_numpy()
+
+
+def test_c3_full_size_every_column(ctx):
+    """C3 at 32768^2: EVERY element vs the correctly-rounded restatement
+    (0 ulp), in 2048-column blocks; the inputs' blocks are re-checked against
+    the reference splitmix64 stream at their offsets."""
+    n, w = 32768, 2048
+    X, Y = fm.randu(n, n, 42, "f32", ctx), fm.randu(n, n, 43, "f32", ctx)
+    Z = fm.Mat(n, n, "f32", ctx)
+    Z.assign(fm.exp(-fm.square(X - Y) / 2) + 0.5 * fm.abs(X))
+    for j0 in range(0, n, w):
+        x, y, z = _block(X, j0, w), _block(Y, j0, w), _block(Z, j0, w)
+        if j0 in (0, n - w):
+            assert np.array_equal(x.ravel(order="F"), orc.uniform_fill(42, n * w, "f32", offset=j0 * n))
+        d = x - y
+        want = (np.exp((np.float32(0.5) * -(d * d)).astype(np.float64)).astype(np.float32)
+                + np.float32(0.5) * np.abs(x))
+        assert orc.max_ulp(z, want) == 0, j0
+
+
+def test_c4_full_size_every_column(ctx):
+    """C4 at 65536 x 16384 f64: every column's sum / mean (within 1e-13 of
+    sum |v|), max and index_max (exact) vs the oracle, in 1024-column blocks."""
+    r, c, w = 65536, 16384, 1024
+    X, Y, Z = (fm.randu(r, c, s, "f64", ctx) for s in (42, 43, 44))
+    e = (X - Y) % Z
+    outs = [fm.Mat(1, c, "f64", ctx), fm.Mat(1, c, "f64", ctx), fm.Mat(1, c, "f64", ctx), fm.Mat(1, c, "u32", ctx)]
+    fm.assign_all([(outs[0], fm.sum(e, 0)), (outs[1], fm.mean(e, 0)), (outs[2], fm.max(e, 0)),
+                   (outs[3], fm.index_max(e, 0))])
+    got = [o.to_numpy() for o in outs]
+    k, f64 = orc.ReduceKind, fm.ElemType.f64
+    for j0 in range(0, c, w):
+        v = (_block(X, j0, w) - _block(Y, j0, w)) * _block(Z, j0, w)
+        sl = slice(j0, j0 + w)
+        # sums of mixed-sign terms can cancel towards 0: bound the error by
+        # the condition of the sum, 1e-13 * sum |v| per column
+        scale = np.abs(v).sum(axis=0, keepdims=True)
+        for o, kind, div in ((0, k.sum, 1.0), (1, k.mean, float(r))):
+            err = np.abs(got[o][:, sl] - orc.reduce_dim(kind, 0, v, f64))
+            assert np.all(err <= 1e-13 * scale / div), (j0, float((err / (scale / div)).max()))
+        assert np.array_equal(got[2][:, sl], orc.reduce_dim(k.max, 0, v, f64)), j0
+        assert np.array_equal(got[3][:, sl], orc.reduce_dim(k.index_max, 0, v, f64)), j0
+
+
+def test_c1_full_size_bit_exact(ctx):
+    """C1 at 4096^2: the whole output bit-exact vs the oracle (the reference's
+    own generated C is 0-ulp against it, tests/test_oracle.py)."""
+    n = 4096
+    X, Y = fm.randu(n, n, 42, "f32", ctx), fm.randu(n, n, 43, "f32", ctx)
+    Z = fm.Mat(n, n, "f32", ctx)
+    Z.assign(2 * (X % Y) + X)
+    x, y = orc.randu(n, n, 42), orc.randu(n, n, 43)
+    assert np.array_equal(Z.to_numpy(), np.float32(2) * (x * y) + x)
