@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ring<E> ring(smem_raw);
   ring.init();
-  pdl_trigger();
-  pdl_wait();
+  const int indep = P.reserved & 1;   // launch-window class (common.cuh)
+  pdl_enter(indep);
   const int warp = threadIdx.x >> 5;
   const int64_t nfull = n_elem / C;
   unsigned *ctr = counters, *done = counters + 1;
@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   }
   // the last CTA out resets the chunk counter for the next launch on this stream
   __syncthreads();
+  if (blockIdx.x == 0) pdl_exit(indep);
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(done, 1u) == gridDim.x - 1) {
@@ -261,8 +262,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   __shared__ bool last;
   Ring<E> ring(smem_raw);
   ring.init();
-  pdl_trigger();
-  pdl_wait();
+  const int indep = P.reserved & 1;   // launch-window class (common.cuh)
+  pdl_enter(indep);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nfull = n_elem / C;
   const int64_t dbase = nstat * gridDim.x;
@@ -332,6 +333,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     last = (atomicAdd(done, 1u) == gridDim.x - 1);
   }
   __syncthreads();
+  if (blockIdx.x == 0) pdl_exit(indep);
   if (!last) return;
   __threadfence();
   // combine: per-CTA partials then per-chunk partials, each thread over a

@@ -24,7 +24,49 @@ struct Scratch {
   void *payload;
   size_t payload_bytes;
 };
-int get_scratch(void *stream, size_t payload_bytes, Scratch *out);
+int get_scratch(void *stream, size_t payload_bytes, Scratch *out, int slot = 0);
+
+// ---- overlap of independent launches (programmatic dependent launch) ------
+// A launch whose byte ranges neither read what an in-flight launch writes
+// nor write what one reads or writes is INDEPENDENT of it.  The library
+// keeps, per stream, the window of launches that may still be running (all
+// launches since the last dependent one, at most kPdlWindow); each PDL launch
+// is classified against it (pdl_classify) and told so through bit 0 of
+// fm_program.reserved:
+//   dependent   -- griddepcontrol.wait, then launch_dependents: everything
+//                  before it has completed before its CTAs do any work, and
+//                  its successor cannot start before that (the window resets);
+//   independent -- launch_dependents at once and NO wait before its work, so
+//                  its CTAs fill SMs the previous kernel's tail leaves idle;
+//                  it waits only before exiting, so its completion still
+//                  implies its predecessors' (later dependent launches stay
+//                  correctly ordered).
+// Each launch in a window gets its own scratch slot (window position), so
+// concurrently running reductions never share partials or counters.
+constexpr int kPdlWindow = 4;
+struct ByteRange {
+  uintptr_t lo, hi;   // [lo, hi)
+};
+struct Footprint {
+  ByteRange rd[FM_MAX_SLOTS];
+  int n_rd = 0;
+  ByteRange wr[FM_MAX_REDUCE_OUT];
+  int n_wr = 0;
+};
+struct PdlPlan {
+  int independent;   // 1: skip the initial wait (fm_program.reserved bit 0)
+  int slot;          // scratch slot of this launch
+};
+PdlPlan pdl_classify(cudaStream_t s, const Footprint &fp);
+// read footprint of a program's slots over an n_rows x n_cols domain
+void program_reads(const fm_program &P, int64_t n_rows, int64_t n_cols, Footprint &fp);
+inline void footprint_write(Footprint &fp, const void *p, size_t bytes) {
+  if (fp.n_wr < FM_MAX_REDUCE_OUT) fp.wr[fp.n_wr++] = {(uintptr_t)p, (uintptr_t)p + bytes};
+}
+
+// kernel side: bit 0 of P.reserved (see above)
+__device__ __forceinline__ void pdl_enter(int independent);
+__device__ __forceinline__ void pdl_exit(int independent);
 // zero-filled plain cudaMalloc made outside any stream capture (safe to call
 // while this thread captures; the address can be baked into a graph)
 int alloc_plain(void **ptr, size_t bytes);
@@ -49,6 +91,17 @@ int launch_copy_program(const fm_program &P, void *out, int64_t n_rows, int64_t 
 bool pdl_enabled();
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter(int independent) {
+  if (independent) {
+    pdl_trigger();
+  } else {
+    pdl_wait();
+    pdl_trigger();
+  }
+}
+__device__ __forceinline__ void pdl_exit(int independent) {
+  if (independent) pdl_wait();
+}
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

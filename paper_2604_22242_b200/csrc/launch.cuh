@@ -16,6 +16,35 @@ namespace fm {
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+inline int etype_bytes(int e) { return e == FM_F64 ? 8 : (e == FM_BF16 ? 2 : 4); }
+
+// Launch-window class of a PDL launch (common.cuh): the program's reads over
+// the domain plus the given writes; returns the program to launch (bit 0 of
+// `reserved` = independent) and the scratch slot.
+struct Classified {
+  fm_program P;
+  int slot;
+};
+inline Classified classify(cudaStream_t s, const fm_program &P0, int64_t n_rows, int64_t n_cols,
+                           const Footprint &writes) {
+  Footprint fp = writes;
+  program_reads(P0, n_rows, n_cols, fp);
+  const PdlPlan pp = pdl_classify(s, fp);
+  Classified c{P0, pp.slot};
+  c.P.reserved = (P0.reserved & ~1) | pp.independent;
+  return c;
+}
+inline Footprint writes_of(const void *out, size_t bytes) {
+  Footprint fp;
+  footprint_write(fp, out, bytes);
+  return fp;
+}
+inline Footprint reduce_writes(const ReduceOuts &R, int64_t n) {
+  Footprint fp;
+  for (int i = 0; i < R.n; ++i) footprint_write(fp, R.o[i].out, (size_t)n * etype_bytes(R.o[i].etype));
+  return fp;
+}
+
 // Resident blocks of `kernel` per SM at kThreads threads (queried once per
 // kernel).  Streaming kernels launch exactly one full wave -- SMs x resident
 // blocks -- and grid-stride: a fractional last wave would leave most SMs idle
@@ -78,10 +107,11 @@ int run_copy_bulk(const fm_program &P, void *out, int64_t n_elem, cudaStream_t s
   }
   const int64_t chunks = n_elem / G::kChunk;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(chunks, sm_count()));
+  const Classified cl = classify(s, P, n_elem, 1, writes_of(out, (size_t)n_elem * etype_bytes(P.result_etype)));
   Scratch sc;
-  int st = get_scratch((void *)s, 64, &sc);
+  int st = get_scratch((void *)s, 64, &sc, cl.slot);
   if (st) return st;
-  FM_CHECK(launch_pdl(bulk::k_copy_bulk<E>, dim3((unsigned)grid), dim3(bulk::kBulkThreads), G::kSmem, s, P, out,
+  FM_CHECK(launch_pdl(bulk::k_copy_bulk<E>, dim3((unsigned)grid), dim3(bulk::kBulkThreads), G::kSmem, s, cl.P, out,
                       n_elem, sc.counters));
   FM_CHECK_LAUNCH("fused copy kernel (bulk)");
   return 0;
@@ -167,7 +197,9 @@ int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cud
   const int64_t nrb = cdiv(n_rows, V);
   const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;
   const int64_t grid = wave_grid<GridTag<E, 0>>(k_copy<E>, cdiv(nch, kThreads));
-  FM_CHECK(launch_pdl(k_copy<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, P, out, n_rows, n_cols));
+  const Classified cl =
+      classify(s, P, n_rows, n_cols, writes_of(out, (size_t)(n_rows * n_cols) * etype_bytes(P.result_etype)));
+  FM_CHECK(launch_pdl(k_copy<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, cl.P, out, n_rows, n_cols));
   FM_CHECK_LAUNCH("fused copy kernel");
   return 0;
 }
@@ -190,11 +222,12 @@ int run_accu_bulk(const fm_program &P, void *out, int64_t n_elem, int finalize, 
   }();
   const int64_t nstat = chunks * static_pct / 100 / grid;
   const int64_t ndyn = chunks - nstat * grid;
+  const Classified cl = classify(s, P, n_elem, 1, writes_of(out, 8));
   Scratch sc;
-  int st = get_scratch((void *)s, (grid + ndyn) * sizeof(double) + 64, &sc);
+  int st = get_scratch((void *)s, (grid + ndyn) * sizeof(double) + 64, &sc, cl.slot);
   if (st) return st;
   double *part_d = (double *)sc.payload;
-  FM_CHECK(launch_pdl(bulk::k_accu_bulk<E>, dim3((unsigned)grid), dim3(bulk::kBulkThreads), G::kSmem, s, P, out,
+  FM_CHECK(launch_pdl(bulk::k_accu_bulk<E>, dim3((unsigned)grid), dim3(bulk::kBulkThreads), G::kSmem, s, cl.P, out,
                       n_elem, finalize, part_d, part_d + grid, nstat, sc.counters));
   FM_CHECK_LAUNCH("fused accu kernel (bulk)");
   return 0;
@@ -215,12 +248,13 @@ int run_accu(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, int
   const int64_t nrb = cdiv(n_rows, V);
   const int64_t nch = P.flat ? cdiv(n_rows * n_cols, V) : nrb * n_cols;
   const int64_t grid = wave_grid<GridTag<E, 1>>(k_accu<E>, cdiv(nch, kThreads));
+  const Classified cl = classify(s, P, n_rows, n_cols, writes_of(out, 8));
   Scratch sc;
-  int st = get_scratch((void *)s, grid * (sizeof(double) + sizeof(uint32_t)) + 64, &sc);
+  int st = get_scratch((void *)s, grid * (sizeof(double) + sizeof(uint32_t)) + 64, &sc, cl.slot);
   if (st) return st;
   double *pd = (double *)sc.payload;
   uint32_t *pu = (uint32_t *)(pd + grid);
-  FM_CHECK(launch_pdl(k_accu<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, P, out, n_rows, n_cols, finalize, pd,
+  FM_CHECK(launch_pdl(k_accu<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, cl.P, out, n_rows, n_cols, finalize, pd,
                       pu, sc.counters));
   FM_CHECK_LAUNCH("fused accu kernel");
   return 0;
@@ -246,14 +280,16 @@ int run_reduce_dim(const fm_program &P, int dim, int64_t n_rows, int64_t n_cols,
         }();
         const int64_t grid = std::min<int64_t>(std::min<int64_t>(n_cols, (int64_t)sm_count() * per_sm),
                                                wave_grid<GridTag<E, 4>>(k_reduce_cols_fast<E>, n_cols));
-        FM_CHECK(launch_pdl(k_reduce_cols_fast<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, P, R, n_rows, n_cols));
+        const fm_program Pc = classify(s, P, n_rows, n_cols, reduce_writes(R, n_cols)).P;
+        FM_CHECK(launch_pdl(k_reduce_cols_fast<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, Pc, R, n_rows, n_cols));
         FM_CHECK_LAUNCH("fused column-reduction kernel (typed)");
         return 0;
       }
     }
     // one persistent wave; columns are the work units (C4: 16384 / 444)
     const int64_t grid = wave_grid<GridTag<E, 2>>(k_reduce_cols<E>, n_cols);
-    FM_CHECK(launch_pdl(k_reduce_cols<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, P, R, n_rows, n_cols));
+    const fm_program Pc = classify(s, P, n_rows, n_cols, reduce_writes(R, n_cols)).P;
+    FM_CHECK(launch_pdl(k_reduce_cols<E>, dim3((unsigned)grid), dim3(kThreads), 0, s, Pc, R, n_rows, n_cols));
     FM_CHECK_LAUNCH("fused column-reduction kernel");
     return 0;
   }

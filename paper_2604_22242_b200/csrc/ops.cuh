@@ -221,11 +221,21 @@ __device__ __forceinline__ float log_f(float a) {
 }
 // tanh of an f32 argument, correctly rounded in practice (f64 evaluation,
 // one rounding): tanh|x| = m / (m + 2) with m = expm1(2|x|) from the same
-// 64-entry exp table (2^(j/64) * (1 + p) - 1: absolute error ~2^-53, relative
-// <= 2^-41 for 2|x| >= 2^-11) and a correctly rounded f64 reciprocal; ~24
-// FP64 operations instead of libdevice tanh's branchy rational forms (the
-// paper's gelu).  |x| < 2^-12 returns x (tanh x = x(1 - x^2/3 + ...) rounds
-// to x); |x| >= 9.1 returns +-1 (1 - tanh|x| < 2^-25).
+// 64-entry exp table (2^(j/64) * (1 + p) - 1: absolute error ~2^-53,
+// relative <= 2^-41 for 2|x| >= 2^-11; for n = 0, m = p itself, so tiny
+// arguments keep full relative accuracy down to subnormals and tanh x
+// rounds to x with no special case) and a branch-free quotient: the
+// hardware's approximate f64 reciprocal of d = m + 2 in [2, 2^28), one
+// Newton step (relative error ~2^-46), the quotient and one residual
+// correction (~2^-53) -- 6 FP64 operations where __drcp_rn + a multiply
+// took 7 plus a range check and branch.  |x| is clamped to 9.5, where the
+// quotient already rounds to 1.0f.  (r01 gelu issue-bound at 66
+// instructions per element, profiles/r02/ncu_gelu.)
+__device__ __forceinline__ double rcp_approx_f64(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  return r;
+}
 __device__ __forceinline__ float tanh_f(float a) {
   const float ax = fabsf(a);
   const double y = 2.0 * (double)fminf(ax, 9.5f);
@@ -242,12 +252,13 @@ __device__ __forceinline__ float tanh_f(float a) {
   const double p = __dmul_rn(q, r);                         // exp(r) - 1
   const double tj = __ldg(&kExp2Tab64[ni & 63]);
   const double sc = __hiloint2double(__double2hiint(tj) + (int)((unsigned)(ni >> 6) << 20), __double2loint(tj));
-  const double m = fma(sc, p, __dsub_rn(sc, 1.0));          // 2^(n/64) (1 + p) - 1
-  const double th = __dmul_rn(m, __drcp_rn(__dadd_rn(m, 2.0)));
-  float res = __double2float_rn(th);
-  if (ax < 0x1p-12f) res = ax;
-  if (ax >= 9.1f) res = 1.0f;
-  res = copysignf(res, a);
+  const double m = fma(sc, p, __dsub_rn(sc, 1.0));          // 2^(n/64) (1 + p) - 1 >= 0
+  const double d = __dadd_rn(m, 2.0);
+  const double r0 = rcp_approx_f64(d);
+  const double r1 = fma(r0, fma(-d, r0, 1.0), r0);          // 1/d to ~2^-46
+  const double q0 = __dmul_rn(m, r1);
+  const double th = fma(r1, fma(-d, q0, m), q0);            // m/d to ~2^-53
+  const float res = copysignf(__double2float_rn(th), a);
   return (a != a) ? a : res;
 }
 __device__ __forceinline__ double exp_d(double a) { return exp(a); }

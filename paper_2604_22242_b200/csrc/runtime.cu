@@ -134,11 +134,11 @@ int pair_order(int64_t n, const uint32_t **table) {
   return 0;
 }
 
-int get_scratch(void *stream, size_t payload_bytes, Scratch *out) {
+int get_scratch(void *stream, size_t payload_bytes, Scratch *out, int slot) {
   int dev = 0;
   FM_CHECK(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_scratch_mu);
-  ScratchEntry &e = g_scratch[{dev, stream}];
+  ScratchEntry &e = g_scratch[{dev * kPdlWindow + slot, stream}];
   if (e.base == nullptr || e.payload < payload_bytes) {
     // grow geometrically; the outgrown block is retired, not freed, because a
     // CUDA graph captured earlier (fm_graph_*) may still hold its address.
@@ -156,6 +156,58 @@ int get_scratch(void *stream, size_t payload_bytes, Scratch *out) {
   out->payload = (char *)e.base + kCounterBytes;
   out->payload_bytes = e.payload;
   return 0;
+}
+
+// ---- launch windows (common.cuh: overlap of independent launches) ----------
+struct PdlWindow {
+  std::vector<Footprint> fps;
+};
+static std::mutex g_pdl_mu;
+static std::map<std::pair<int, void *>, PdlWindow> g_pdl;
+
+static bool overlaps(const ByteRange *a, int na, const ByteRange *b, int nb) {
+  for (int i = 0; i < na; ++i)
+    for (int j = 0; j < nb; ++j)
+      if (a[i].lo < b[j].hi && b[j].lo < a[i].hi) return true;
+  return false;
+}
+
+// forget the stream's window (graph boundaries: the launches around a
+// capture are not each other's neighbours when the graph replays)
+static void pdl_reset(void *stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  g_pdl.erase({dev, stream});
+}
+
+PdlPlan pdl_classify(cudaStream_t s, const Footprint &fp) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  PdlWindow &w = g_pdl[{dev, (void *)s}];
+  bool indep = pdl_enabled() && !w.fps.empty() && (int)w.fps.size() < kPdlWindow && fp.n_wr > 0;
+  for (size_t i = 0; indep && i < w.fps.size(); ++i) {
+    const Footprint &o = w.fps[i];
+    if (overlaps(fp.rd, fp.n_rd, o.wr, o.n_wr) || overlaps(fp.wr, fp.n_wr, o.rd, o.n_rd) ||
+        overlaps(fp.wr, fp.n_wr, o.wr, o.n_wr))
+      indep = false;
+  }
+  if (!indep) w.fps.clear();
+  w.fps.push_back(fp);
+  return PdlPlan{indep ? 1 : 0, (int)w.fps.size() - 1};
+}
+
+void program_reads(const fm_program &P, int64_t n_rows, int64_t n_cols, Footprint &fp) {
+  for (int j = 0; j < P.n_slots; ++j) {
+    const fm_slot &sl = P.slots[j];
+    const int w = sl.etype == FM_F64 ? 8 : (sl.etype == FM_BF16 ? 2 : 4);
+    int64_t r = n_rows, c = n_cols;
+    if (sl.transposed) std::swap(r, c);
+    if (sl.map == FM_MAP_DIAG) c = r;
+    const int64_t last = (sl.row_off + std::max<int64_t>(r, 1) - 1) + (sl.col_off + std::max<int64_t>(c, 1) - 1) * sl.ld;
+    fp.rd[fp.n_rd++] = {(uintptr_t)sl.ptr, (uintptr_t)sl.ptr + (uintptr_t)((last + 1) * w)};
+  }
 }
 
 // ---- graph-owned allocations ---------------------------------------------
@@ -408,6 +460,7 @@ struct FmGraph {
 int fm_graph_begin(void *stream) {
   if (g_capture.active) return fail_msg("graph_begin: this thread is already capturing");
   FM_CHECK(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
+  pdl_reset(stream);
   g_capture.active = true;
   g_capture.ptrs.clear();
   return 0;
@@ -419,6 +472,7 @@ int fm_graph_end(void *stream, void **graph, int64_t *kernels) {
   std::vector<void *> owned;
   owned.swap(g_capture.ptrs);
   cudaError_t ce = cudaStreamEndCapture((cudaStream_t)stream, &g);
+  pdl_reset(stream);
   if (ce != cudaSuccess) {
     owned_release_refs(owned);
     return fail("cudaStreamEndCapture", ce);
@@ -449,6 +503,7 @@ int fm_graph_launch(void *graph, void *stream) {
   if (!graph) return fail_msg("graph_launch: null graph");
   FmGraph *fg = (FmGraph *)graph;
   FM_CHECK(cudaGraphLaunch(fg->exec, (cudaStream_t)stream));
+  pdl_reset(stream);
   count_launch(fg->kernels);
   return 0;
 }

@@ -127,8 +127,8 @@ template <class E>
 __global__ void __launch_bounds__(kThreads, E::kMinBlocks) k_copy(const __grid_constant__ fm_program P, void *out,
                                                    int64_t n_rows, int64_t n_cols) {
   constexpr int V = E::kV;
-  pdl_trigger();
-  pdl_wait();
+  const int indep = P.reserved & 1;   // launch-window class (common.cuh)
+  pdl_enter(indep);
   const int64_t n_elem = n_rows * n_cols;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, E::kMinBlocks) k_copy(const __grid_c
     E::eval(P, ch, lo, hi);
     store_chunk<V>(out, P.result_etype, ch.base, ch.cnt, lo, hi);
   }
+  if (blockIdx.x == 0) pdl_exit(indep);
 }
 
 // ---- block reductions ------------------------------------------------------------------------
@@ -270,8 +271,8 @@ __global__ void __launch_bounds__(kThreads) k_accu(const __grid_constant__ fm_pr
   __shared__ bool last;
   const int rt = P.result_etype;
   const bool fl = is_float_etype(rt);
-  pdl_trigger();
-  pdl_wait();
+  const int indep = P.reserved & 1;   // launch-window class (common.cuh)
+  pdl_enter(indep);
   int64_t nrb;
   const int64_t nch = chunk_count<V>(P, n_rows, n_cols, nrb);
   const int64_t n_elem = n_rows * n_cols;
@@ -320,6 +321,7 @@ __global__ void __launch_bounds__(kThreads) k_accu(const __grid_constant__ fm_pr
     last = (t == gridDim.x - 1);
   }
   __syncthreads();
+  if (blockIdx.x == 0) pdl_exit(indep);
   if (!last) return;
   __threadfence();
   double sd = 0.0;
@@ -486,8 +488,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_reduce_cols(const __grid_consta
   const int rt = P.result_etype;
   const bool fl = is_float_etype(rt);
   const unsigned need = needed_stats(R);
-  pdl_trigger();
-  pdl_wait();
+  const int indep = P.reserved & 1;   // launch-window class (common.cuh)
+  pdl_enter(indep);
   bool fast = false;
   int64_t fast_rows = 0;
   if constexpr (E::kFast) {
@@ -538,6 +540,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_reduce_cols(const __grid_consta
       for (int i = 0; i < R.n; ++i) emit_out(R.o[i], col, t, rt, fl, n_rows);
     __syncthreads();
   }
+  if (blockIdx.x == 0) pdl_exit(indep);
 }
 
 // dim 0, typed fast path only: every column is a whole number of warp tiles
@@ -556,8 +559,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_reduce_cols_fast(const __grid_c
   __shared__ Cand smc[kThreads / 32];
   const int rt = P.result_etype;
   const unsigned need = needed_stats(R);
-  pdl_trigger();
-  pdl_wait();
+  const int indep = P.reserved & 1;   // launch-window class (common.cuh)
+  pdl_enter(indep);
   const int lane = threadIdx.x & 31;
   const int64_t ntile = n_rows / kTile;
   for (int64_t col = blockIdx.x; col < n_cols; col += gridDim.x) {
@@ -590,6 +593,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_reduce_cols_fast(const __grid_c
       for (int i = 0; i < R.n; ++i) emit_out(R.o[i], col, tt, rt, true, n_rows);
     __syncthreads();
   }
+  if (blockIdx.x == 0) pdl_exit(indep);
 }
 
 // General chunk path of a row run over columns [c0, c1): out of line so the

@@ -5,7 +5,7 @@ bench.py reads this file for roofline.traffic.  A label maps to the capture of
 the kernel instantiation it launches (dot_X launches the same k_accu<Mul<..>>
 instantiation as accu_schur_X, so they share a capture).
 
-    python scripts/make_traffic.py [round-dir ...]   (default: profiles/r01)
+    python scripts/make_traffic.py [round-dir ...]   (default: profiles/r02, then profiles/r01 for labels r02 lacks)
 """
 import csv
 import json
@@ -27,6 +27,7 @@ LABELS = {
     "c5_gemm_bf16": "ncu_c5_gemm",
     "c5_gemm_f32": "ncu_c5f32_gemm",
     "expr1": "ncu_suite_expr1",
+    "expr2": "ncu_suite_expr2",
 }
 
 
@@ -54,4 +55,4 @@ def main(dirs):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["profiles/r01"])
+    main(sys.argv[1:] or ["profiles/r01", "profiles/r02"])

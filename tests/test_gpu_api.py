@@ -501,3 +501,78 @@ def test_tanh_f32_sweep_vs_correctly_rounded(ctx):
     assert np.array_equal(np.signbit(got[ok]), np.signbit(want[ok]))     # tanh(-0) = -0
     diff = np.count_nonzero(got[ok].view(np.uint32) != want[ok].view(np.uint32))
     assert diff <= max(4, len(x) // 1_000_000), diff
+
+
+# ---- launch windows (common.cuh): independent launches overlap through
+# programmatic dependent launch; dependent ones wait.  Results must not change.
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_overlapping_independent_launches(ctx, graph):
+    n = 1 << 22
+    X = fm.randu(n, 1, 301, "f32", ctx)
+    Y = fm.randu(n, 1, 302, "f32", ctx)
+    W = fm.randu(n, 1, 303, "f64", ctx)
+    A = fm.Mat(n, 1, "f32", ctx)
+    B = fm.Mat(n, 1, "f32", ctx)
+    C = fm.Mat(n, 1, "f64", ctx)
+    outs = {}
+
+    R = fm.Mat(4, 1, "f64", ctx)
+
+    def step():
+        # independent reductions and copies (a window holds 4 launches: the
+        # 5th independent one waits), copies reading each other's outputs
+        # (dependent), in-place updates
+        fm.dot_async(X, Y, R, 0)
+        A.assign(X + Y)                     # independent of X.Y
+        fm.accu_async(W, R, 1)              # independent
+        B.assign(A * 2.0)                   # reads A: dependent
+        C.assign(W * 3.0)                   # independent of B
+        fm.accu_async(X, R, 2)
+        A.assign(B - X)                     # reads B, writes A (read by B's launch)
+        C.assign(C + 1.0)                   # in place on C
+        fm.accu_async(C, R, 3)              # reads C just written
+
+    x, y, w = X.to_numpy(), Y.to_numpy(), W.to_numpy()
+    if graph:
+        g = fm.capture(step, ctx)
+        for _ in range(3):
+            C.assign(W * 0.0)
+            ctx.sync()
+            g.replay()
+        ctx.sync()
+        g.close()
+    else:
+        for _ in range(3):
+            step()
+    b = (x + y) * np.float32(2.0)
+    assert np.array_equal(B.to_numpy(), b)
+    assert np.array_equal(A.to_numpy(), b - x)
+    c = w * 3.0 + 1.0
+    assert np.array_equal(C.to_numpy(), c)
+    r = R.to_numpy().ravel()
+    want = [orc.accu(x * y, fm.ElemType.f32), orc.accu(w, fm.ElemType.f64), orc.accu(x, fm.ElemType.f32),
+            orc.accu(c, fm.ElemType.f64)]
+    assert r == pytest.approx(want, rel=1e-12)
+
+
+def test_back_to_back_reductions_share_no_scratch(ctx):
+    """Many independent full reductions in a row (each its own scratch slot
+    within a window) give the same sums as one at a time."""
+    n = 3_000_000
+    vs = [fm.randu(n, 1, 400 + i, "f64", ctx) for i in range(9)]
+    want = [fm.accu(v) for v in vs]           # one at a time (synchronising)
+    for _ in range(3):
+        outs = [fm.Mat(1, 1, "f64", ctx) for _ in vs]
+        fm.assign_all([(o, fm.sum(v, 0)) for o, v in zip(outs, vs)])
+        ctx.sync()
+        got = [float(o.to_numpy()[0, 0]) for o in outs]
+        assert got == pytest.approx(want, rel=1e-13)
+    R = fm.Mat(len(vs), 1, "f64", ctx)
+    g = fm.capture(lambda: [fm.accu_async(v, R, i) for i, v in enumerate(vs)], ctx)
+    for _ in range(3):
+        R.assign(R * 0.0)
+        g.replay()
+        ctx.sync()
+        assert list(R.to_numpy().ravel()) == pytest.approx(want, rel=1e-13)
+    g.close()
