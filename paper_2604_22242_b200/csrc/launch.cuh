@@ -295,12 +295,33 @@ int run_reduce_dim(const fm_program &P, int dim, int64_t n_rows, int64_t n_cols,
   }
   const int64_t gx = cdiv(n_rows, (int64_t)kThreads * V);
   if (gx > 65535 * 1024LL) return fail_msg("reduce_dim: too many rows");
-  static const int64_t per_sm = [] {
+  // typed fast path: a TMA-bulk ring of `depth` columns per block (the
+  // deepest of 8..3 that still fits two CTAs per SM)
+  int depth = 0;
+  size_t smem = 0;
+  if constexpr (E::kFast) {
+    using T = typename E::Elem;
+    if (host_fast_ok<E>(P, nullptr) && ((n_rows * (int64_t)sizeof(T)) & 15) == 0 && n_rows % (kThreads * V) == 0) {
+      const size_t per_col = (size_t)E::kNin * E::kV * sizeof(T) * kThreads;
+      for (int d = 8; d >= 3; --d)
+        if (d * per_col + 8 * d <= 100 * 1024) { depth = d; break; }
+      smem = depth * per_col + 8 * (size_t)depth;
+      static bool attr = false;
+      if (depth && !attr) {
+        FM_CHECK(cudaFuncSetAttribute(k_reduce_rows<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        attr = true;
+      }
+    }
+  }
+  // column splits so enough CTAs per SM stream concurrently: c4r (65536 x
+  // 16384 f64), register path 2 -> 4.74, 4 -> 5.80, 8 -> 6.13, 16 -> 6.37,
+  // 32 -> 5.95 TB/s; staged path 2 -> 5.93, 4 -> 6.67, 6 -> 6.76,
+  // 8 -> 6.79, 16 -> 6.44 (longer column runs per CTA)
+  static const int64_t per_sm_env = [] {
     const char *e = getenv("FMB200_ROW_SPLITS_PER_SM");
-    return (int64_t)((e && *e) ? std::max(1, atoi(e)) : 16);
+    return (int64_t)((e && *e) ? std::max(1, atoi(e)) : 0);
   }();
-  // column splits so ~16 CTAs per SM stream concurrently (c4r, 65536 x 16384
-  // f64: 2 -> 4.74, 4 -> 5.80, 8 -> 6.13, 16 -> 6.37, 32 -> 5.95 TB/s)
+  const int64_t per_sm = per_sm_env ? per_sm_env : (depth ? 8 : 16);
   int64_t splits = std::max<int64_t>(1, cdiv((int64_t)sm_count() * per_sm, gx));
   splits = std::min<int64_t>(splits, std::min<int64_t>(n_cols, 65535));
   RowPartial *part = nullptr;
@@ -314,7 +335,7 @@ int run_reduce_dim(const fm_program &P, int dim, int64_t n_rows, int64_t n_cols,
     counters = sc.counters;
   }
   dim3 grid((unsigned)gx, (unsigned)splits);
-  k_reduce_rows<E><<<grid, kThreads, 0, s>>>(P, R, n_rows, n_cols, part, counters);
+  k_reduce_rows<E><<<grid, kThreads, smem, s>>>(P, R, n_rows, n_cols, part, counters, depth);
   FM_CHECK_LAUNCH("fused row-reduction kernel");
   return 0;
 }

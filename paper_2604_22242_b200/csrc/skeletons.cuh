@@ -624,11 +624,48 @@ struct RowPartial {
   Cand mx, mn;
 };
 
+// mbarrier + TMA bulk copy helpers of the staged row reduction
+FM_DEV uint32_t smem_addr_rows(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+FM_DEV void mbar_init_rows(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr_rows(bar)), "r"(count));
+}
+FM_DEV void mbar_arrive_expect_tx_rows(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr_rows(bar)), "r"(bytes)
+               : "memory");
+}
+FM_DEV void mbar_wait_rows(uint64_t *bar, uint32_t parity) {
+  const uint32_t a = smem_addr_rows(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+FM_DEV void bulk_g2s_rows(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr_rows(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr_rows(bar))
+      : "memory");
+}
+
+// `depth` > 0: the typed fast path streams its columns through a shared-
+// memory ring of `depth` stages filled by TMA bulk copies (one per input and
+// column: the block's rows of a column are contiguous), so `depth` columns
+// are in flight without holding registers.  The register version (one
+// column ahead) kept ~50 KB in flight per SM at 25 % occupancy and ran
+// long-scoreboard-bound at 6.34 TB/s (profiles/r02/ncu_c4r_rowstats); a
+// per-thread cp.async ring was MIO-throttled (3.8 TB/s).
 template <class E>
 __global__ void __launch_bounds__(kThreads) k_reduce_rows(const __grid_constant__ fm_program P,
                                                           const __grid_constant__ ReduceOuts R,
                                                           int64_t n_rows, int64_t n_cols,
-                                                          RowPartial *part, unsigned *counters) {
+                                                          RowPartial *part, unsigned *counters, int depth) {
   constexpr int V = E::kV;
   __shared__ bool last;
   const int rt = P.result_etype;
@@ -657,6 +694,61 @@ __global__ void __launch_bounds__(kThreads) k_reduce_rows(const __grid_constant_
       ColStats<T> cs[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) cs[v].init();
+      auto fold = [&](const uint4 (&b)[NIN][NQ], int64_t col) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+          for (int e = 0; e < kW; ++e) {
+            T x[NIN];
+#pragma unroll
+            for (int i = 0; i < NIN; ++i) {
+              if constexpr (sizeof(T) == 8) x[i] = e == 0 ? u2d(b[i][q].x, b[i][q].y) : u2d(b[i][q].z, b[i][q].w);
+              else x[i] = u2f(e == 0 ? b[i][q].x : e == 1 ? b[i][q].y : e == 2 ? b[i][q].z : b[i][q].w);
+            }
+            cs[q * kW + e].add(E::ev_elem(P, x), (uint32_t)col, need);
+          }
+      };
+      if (depth > 0) {
+        // ring of `depth` stages; stage d holds, per input, this CTA's
+        // kThreads * V rows of one column (contiguous in HBM: one TMA bulk
+        // copy each, completion counted on full[d]); thread 0 refills a
+        // stage once the whole block has read it
+        extern __shared__ __align__(128) unsigned char rring[];
+        constexpr int kSeg = kThreads * V * (int)sizeof(T);      // bytes per input per column
+        uint64_t *full = (uint64_t *)(rring + (size_t)depth * NIN * kSeg);
+        const int64_t rows_here = min((int64_t)kThreads * V, n_rows - (int64_t)blockIdx.x * kThreads * V);
+        const uint32_t seg_bytes = (uint32_t)(rows_here * (int64_t)sizeof(T));
+        auto issue = [&](int64_t col, int d) {
+          mbar_arrive_expect_tx_rows(&full[d], seg_bytes * NIN);
+#pragma unroll
+          for (int i = 0; i < NIN; ++i)
+            bulk_g2s_rows(rring + (size_t)(d * NIN + i) * kSeg,
+                          (const T *)P.slots[i].ptr + col * n_rows + (int64_t)blockIdx.x * kThreads * V, seg_bytes,
+                          &full[d]);
+        };
+        if (threadIdx.x == 0) {
+          for (int d = 0; d < depth; ++d) mbar_init_rows(&full[d], 1);
+          asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+          for (int d = 0; d < depth; ++d)
+            if (c0 + d < c1) issue(c0 + d, d);
+        }
+        __syncthreads();
+        int d = 0;
+        uint32_t ph = 0;
+        for (int64_t col = c0; col < c1; ++col) {
+          mbar_wait_rows(&full[d], ph);
+          uint4 b[NIN][NQ];
+#pragma unroll
+          for (int i = 0; i < NIN; ++i)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+              b[i][q] = *(const uint4 *)(rring + (size_t)(d * NIN + i) * kSeg + (size_t)threadIdx.x * V * sizeof(T) + 16 * q);
+          __syncthreads();   // stage d read by the whole block
+          if (threadIdx.x == 0 && col + depth < c1) issue(col + depth, d);
+          fold(b, col);
+          if (++d == depth) { d = 0; ph ^= 1u; }
+        }
+      } else {
       uint4 cur[NIN][NQ], nxt[NIN][NQ];
       auto load = [&](int64_t col, uint4 (&b)[NIN][NQ]) {
 #pragma unroll
@@ -669,22 +761,12 @@ __global__ void __launch_bounds__(kThreads) k_reduce_rows(const __grid_constant_
       if (c0 < c1) load(c0, cur);
       for (int64_t col = c0; col < c1; ++col) {
         if (col + 1 < c1) load(col + 1, nxt);
-#pragma unroll
-        for (int q = 0; q < NQ; ++q)
-#pragma unroll
-          for (int e = 0; e < kW; ++e) {
-            T x[NIN];
-#pragma unroll
-            for (int i = 0; i < NIN; ++i) {
-              if constexpr (sizeof(T) == 8) x[i] = e == 0 ? u2d(cur[i][q].x, cur[i][q].y) : u2d(cur[i][q].z, cur[i][q].w);
-              else x[i] = u2f(e == 0 ? cur[i][q].x : e == 1 ? cur[i][q].y : e == 2 ? cur[i][q].z : cur[i][q].w);
-            }
-            cs[q * kW + e].add(E::ev_elem(P, x), (uint32_t)col, need);
-          }
+        fold(cur, col);
 #pragma unroll
         for (int i = 0; i < NIN; ++i)
 #pragma unroll
           for (int q = 0; q < NQ; ++q) cur[i][q] = nxt[i][q];
+      }
       }
 #pragma unroll
       for (int v = 0; v < V; ++v) cs[v].to_stats(s[v]);
