@@ -374,5 +374,124 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   }
 }
 
+// ---- register VM over bulk-staged chunks (flat programs) ----------------------
+// The VM's chunk path keeps only its prefetched slots in flight per thread;
+// with ~158 registers one 256-thread CTA fits an SM and C1 on the VM ran at
+// 2.0 TB/s, 22 % DRAM, 23 % issue (profiles/r02/ncu_vm_c1).  Here a producer
+// lane streams chunks of EVERY slot (any element widths, chunk_elems
+// elements each) into a ring with TMA bulk copies, chunks claimed
+// dynamically, and kVmWarps consumer warps run the VM out of shared memory
+// (Chunk::bstage: slot j's data at stage + slot.reserved), storing straight
+// to HBM.  Memory parallelism no longer depends on the VM's register use.
+constexpr int kVmWarps = 16;
+constexpr int kVmThreads = (kVmWarps + 1) * 32;
+
+template <class E>
+__global__ void __launch_bounds__(kVmThreads, 1)
+    k_copy_bulk_vm(const __grid_constant__ fm_program P, void *out, int64_t n_elem, unsigned *counters,
+                   int chunk_elems, int stages, int stage_bytes) {
+  constexpr int V = E::kV;
+  extern __shared__ __align__(128) unsigned char vsm[];
+  uint64_t *full = (uint64_t *)(vsm + (size_t)stages * stage_bytes);
+  uint64_t *empty = full + stages;
+  int64_t *cid = (int64_t *)(empty + stages);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kVmWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int indep = P.reserved & 1;   // launch-window class (common.cuh)
+  pdl_enter(indep);
+  const int warp = threadIdx.x >> 5;
+  const int64_t nfull = n_elem / chunk_elems;
+  unsigned *ctr = counters, *done = counters + 1;
+  if (warp == kVmWarps) {
+    if ((threadIdx.x & 31) == 0) {
+      const uint64_t pol = evict_first_policy();
+      int64_t k = 0;
+      auto stage_for = [&](int64_t kk) {
+        const int st = (int)(kk % stages);
+        if (kk >= stages) mbar_wait(&empty[st], (uint32_t)(((kk / stages) & 1) ^ 1));
+        return st;
+      };
+      auto issue = [&](int64_t c) {
+        const int st = stage_for(k++);
+        cid[st] = c;
+        mbar_expect_tx(&full[st], (uint32_t)stage_bytes);
+        for (int j = 0; j < P.n_slots; ++j) {
+          const fm_slot &sl = P.slots[j];
+          const int w = sl.etype == FM_F64 ? 8 : (sl.etype == FM_BF16 ? 2 : 4);
+          bulk_g2s(vsm + (size_t)st * stage_bytes + sl.reserved, (const unsigned char *)sl.ptr + c * chunk_elems * w,
+                   (uint32_t)chunk_elems * w, &full[st], pol);
+        }
+      };
+      // a static head of the chunks round-robin (no claim round trip per
+      // chunk: 148 producers on one counter made the claim the bottleneck),
+      // the rest claimed dynamically so fast SMs take more
+      const int64_t nstat = nfull * 3 / 4 / gridDim.x;
+      for (int64_t j = 0; j < nstat; ++j) issue(blockIdx.x + j * gridDim.x);
+      const int64_t dbase = nstat * gridDim.x;
+      int64_t c = dbase + atomicAdd(ctr, 1u);
+      while (c < nfull) {
+        const int64_t next = dbase + atomicAdd(ctr, 1u);
+        issue(c);
+        c = next;
+      }
+      const int st = stage_for(k);
+      cid[st] = -1;
+      mbar_arrive(&full[st]);
+    }
+  } else {
+    const int ctid = threadIdx.x;
+    const int groups = chunk_elems / V;
+    for (int64_t k = 0;; ++k) {
+      const int st = (int)(k % stages);
+      mbar_wait(&full[st], (uint32_t)((k / stages) & 1));
+      const int64_t c = cid[st];
+      if (c < 0) break;
+      for (int g = ctid; g < groups; g += kVmWarps * 32) {
+        Chunk ch;
+        ch.flat = true;
+        ch.base = c * chunk_elems + (int64_t)g * V;
+        ch.cnt = V;
+        ch.row0 = 0;
+        ch.col = 0;
+        ch.bstage = vsm + (size_t)st * stage_bytes;
+        ch.boff = g * V;
+        uint32_t lo[V], hi[V];
+        E::eval(P, ch, lo, hi);
+        store_chunk<V>(out, P.result_etype, ch.base, V, lo, hi);
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[st]);
+    }
+    // ragged tail (< one chunk): block 0, the VM's global-memory path
+    if (blockIdx.x == 0) {
+      for (int64_t e0 = nfull * chunk_elems + (int64_t)ctid * V; e0 < n_elem; e0 += (int64_t)kVmWarps * 32 * V) {
+        Chunk ch;
+        ch.base = e0;
+        ch.cnt = (int)min((int64_t)V, n_elem - e0);
+        ch.row0 = 0; ch.col = 0; ch.flat = true;
+        uint32_t lo[V], hi[V];
+        E::eval(P, ch, lo, hi);
+        store_chunk<V>(out, P.result_etype, ch.base, ch.cnt, lo, hi);
+      }
+    }
+  }
+  // the last CTA out resets the chunk counter for the next launch on this slot
+  __syncthreads();
+  if (blockIdx.x == 0) pdl_exit(indep);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      *ctr = 0u;
+      *done = 0u;
+    }
+  }
+}
+
 }  // namespace bulk
 }  // namespace fm

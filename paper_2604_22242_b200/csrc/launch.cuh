@@ -117,6 +117,48 @@ int run_copy_bulk(const fm_program &P, void *out, int64_t n_elem, cudaStream_t s
   return 0;
 }
 
+// Register VM over bulk-staged chunks (bulk.cuh k_copy_bulk_vm): a flat
+// program of <= 8 leaf slots, 16-byte aligned, large enough for a wave of
+// chunks.  handled = false: not eligible.
+template <class E>
+int run_copy_bulk_vm(const fm_program &P0, void *out, int64_t n_elem, cudaStream_t s, bool &handled) {
+  handled = false;
+  if (!P0.flat || P0.n_slots < 1 || P0.n_slots > 8) return 0;
+  fm_program P = P0;
+  int bytes_per_elem = 0;
+  for (int j = 0; j < P.n_slots; ++j) {
+    const fm_slot &sl = P.slots[j];
+    if (((uintptr_t)sl.ptr) & 15) return 0;
+    bytes_per_elem += etype_bytes(sl.etype);
+  }
+  // 4 stages in <= 200 KiB; 256-element granules keep every slot's run a
+  // 16-byte multiple (TMA bulk copies)
+  const int chunk = (200 * 1024 / 4 / bytes_per_elem) / 256 * 256;
+  if (chunk < 256 || n_elem < (int64_t)chunk * sm_count()) return 0;
+  int off = 0;
+  for (int j = 0; j < P.n_slots; ++j) {   // slot j's run inside a stage
+    P.slots[j].reserved = off;
+    off += chunk * etype_bytes(P.slots[j].etype);
+  }
+  const int stage_bytes = off, stages = 4;
+  const size_t smem = (size_t)stages * stage_bytes + (size_t)stages * 24 + 64;
+  static bool attr = false;
+  if (!attr) {
+    FM_CHECK(cudaFuncSetAttribute(bulk::k_copy_bulk_vm<typename NoPrefetch<E>::type>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    attr = true;
+  }
+  const Classified cl = classify(s, P, n_elem, 1, writes_of(out, (size_t)n_elem * etype_bytes(P.result_etype)));
+  Scratch sc;
+  if (int st = get_scratch((void *)s, 64, &sc, cl.slot)) return st;
+  const int64_t grid = std::min<int64_t>(n_elem / chunk, sm_count());
+  FM_CHECK(launch_pdl(bulk::k_copy_bulk_vm<typename NoPrefetch<E>::type>, dim3((unsigned)grid), dim3(bulk::kVmThreads),
+                      smem, s, cl.P, out, n_elem, sc.counters, chunk, stages, stage_bytes));
+  FM_CHECK_LAUNCH("fused copy kernel (VM, bulk-staged)");
+  handled = true;
+  return 0;
+}
+
 // Tiled, shared-memory staged VM copy (tiled.cuh): the widest column tile
 // whose double-buffered slot tiles fit in shared memory.
 template <class E, int TC>
@@ -185,6 +227,11 @@ int run_copy(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, cud
       if (handled) return 0;
     }
     if (tiled_enabled() && transposed && n_rows * n_cols >= 4096) return run_copy_tiled<E>(P, out, n_rows, n_cols, s);
+  }
+  if constexpr (E::kIsVm) {
+    bool handled = false;
+    if (int st = run_copy_bulk_vm<E>(P, out, n_rows * n_cols, s, handled)) return st;
+    if (handled) return 0;
   }
   if constexpr (E::kFast) {
     if constexpr (bulk::Geometry<E>::kOk) {

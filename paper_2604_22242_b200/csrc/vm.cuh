@@ -70,6 +70,11 @@ struct Chunk {
   // 3: a diagonal tile), and the bytes of one staged 32 x 32 tile
   int pair = 0;
   int tile_bytes = 0;
+  // bulk-staged flat chunk (bulk.cuh k_copy_bulk_vm): slot j's elements of
+  // the staged chunk start at bstage + slot.reserved; this chunk's first
+  // element is element `boff` of it
+  const unsigned char *bstage = nullptr;
+  int boff = 0;
 };
 
 // Load V elements of slot s for a flat chunk (every slot dense, same shape).
@@ -260,6 +265,38 @@ FM_DEV void load_pair(const fm_slot &s, const Chunk &ch, uint32_t (&lo)[V], uint
   }
 }
 
+// V elements of slot s from a bulk-staged chunk (vector shared-memory loads)
+template <int V>
+FM_DEV void load_bulk(const fm_slot &s, const Chunk &ch, uint32_t (&lo)[V], uint32_t (&hi)[V]) {
+  const unsigned char *p = ch.bstage + s.reserved;
+  if (s.etype == FM_F64) {
+    p += (size_t)ch.boff * 8;
+#pragma unroll
+    for (int q = 0; q < V / 2; ++q) {
+      const uint4 x = *(const uint4 *)(p + 16 * q);
+      lo[2 * q] = x.x; hi[2 * q] = x.y; lo[2 * q + 1] = x.z; hi[2 * q + 1] = x.w;
+    }
+  } else if (s.etype == FM_BF16) {
+    p += (size_t)ch.boff * 2;
+    if constexpr (V == 8) {
+      const uint4 x = *(const uint4 *)p;
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { lo[2 * q] = w[q] << 16; lo[2 * q + 1] = w[q] & 0xffff0000u; }
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) lo[v] = ((uint32_t)((const uint16_t *)p)[v]) << 16;
+    }
+  } else {
+    p += (size_t)ch.boff * 4;
+#pragma unroll
+    for (int q = 0; q < V / 4; ++q) {
+      const uint4 x = *(const uint4 *)(p + 16 * q);
+      lo[4 * q] = x.x; lo[4 * q + 1] = x.y; lo[4 * q + 2] = x.z; lo[4 * q + 3] = x.w;
+    }
+  }
+}
+
 // Slot j of the program for the chunk: staged tile when the kernel staged it
 // (every slot but diagonals), global memory otherwise.
 template <int V, bool FLAT_ONLY = false>
@@ -270,7 +307,8 @@ FM_DEV void fetch_slot(const fm_program &P, int j, const Chunk &ch, uint32_t (&l
     // carry no view / staging code: fewer live registers
     load_slot_flat<V>(s, ch, lo, hi);
   } else {
-    if (ch.pair) load_pair<V>(s, ch, lo, hi);
+    if (ch.bstage) load_bulk<V>(s, ch, lo, hi);
+    else if (ch.pair) load_pair<V>(s, ch, lo, hi);
     else if (ch.stage && s.map != FM_MAP_DIAG) load_staged<V>(s, ch.stage + (size_t)j * ch.slot_bytes, ch, lo, hi);
     else load_slot<V>(s, ch, lo, hi);
   }
@@ -289,14 +327,14 @@ struct Vm {
   static constexpr bool kFast = false;
   FM_DEV static bool fast_ok(const fm_program &, const void *) { return false; }
   static constexpr int HD = WIDE ? MAXD : 1;
-  static constexpr int HP = WIDE ? NPF : 1;
+  static constexpr int HP = WIDE && NPF > 0 ? NPF : 1;
 
   // Evaluate the chunk; result bits land in (lo0, hi0).
   FM_DEV static void eval(const fm_program &P, const Chunk &ch, uint32_t (&lo0)[V], uint32_t (&hi0)[V]) {
     uint32_t lo[MAXD][V];
     uint32_t hi[HD][V];
-    uint32_t plo[NPF][V];
-    uint32_t phi[HP][V];
+    uint32_t plo[NPF > 0 ? NPF : 1][V];
+    uint32_t phi[HP > 0 ? HP : 1][V];
 
     // Prefetch: all loads issued back to back.
 #pragma unroll
@@ -479,5 +517,11 @@ struct Vm {
 #undef ALLD
   }
 };
+
+// The same VM without prefetched slots: for kernels whose slots come from
+// shared memory (bulk.cuh k_copy_bulk_vm) a PUSH is a short LDS, and the
+// prefetch registers (NPF x V words) only cost occupancy.
+template <class E> struct NoPrefetch { using type = E; };
+template <bool W, int D, int V, int N> struct NoPrefetch<Vm<W, D, V, N>> { using type = Vm<W, D, V, 0>; };
 
 }  // namespace fm

@@ -41,4 +41,4 @@ cases = [("c1 2*(X%Y)+X", lambda X, Y: 2 * (X % Y) + X, 2),
 for name, build, nin in cases:
     t = gbs(True, build, nin)
     v = gbs(False, build, nin)
-    print(f"{name:14s} template {t:8.1f} GB/s   VM {v:8.1f} GB/s   VM/template {v / t:.2f}")
+    print(f"{name:14s} template {t:8.1f} GB/s   VM {v:8.1f} GB/s   VM/template {v / t:.2f}", flush=True)

@@ -170,3 +170,36 @@ def test_norm_and_dot_pinned_to_reference(gpu_ctx, golden_cases):
         assert abs(fm.norm(x - y) ** 2 - normsq) <= 1e-12 * normsq
         assert abs(fm.dot(x, y) - dot) <= 1e-12 * dot
         assert abs(fm.accu((x - y) ** 2) - normsq) <= 1e-12 * normsq
+
+
+# ---- the register VM over bulk-staged chunks (bulk.cuh k_copy_bulk_vm):
+# flat programs large enough for a wave of chunks, every slot width, a ragged
+# tail, against the template path / numpy on the same inputs
+
+@pytest.fixture(scope="module")
+def vm_ctx(gpu_ctx):
+    return fm.Context(fm.B200Backend(use_templates=False))
+
+
+@pytest.mark.parametrize("n_rows,n_cols", [(2048, 1024), (3001, 997)])
+def test_vm_bulk_staged_copies(vm_ctx, n_rows, n_cols):
+    ctx = vm_ctx
+    X = fm.randu(n_rows, n_cols, 11, "f32", ctx)
+    Y = fm.randu(n_rows, n_cols, 12, "f32", ctx)
+    D = fm.randu(n_rows, n_cols, 13, "f64", ctx)
+    U = fm.randi(n_rows, n_cols, 50, 14, "u32", ctx)
+    B = fm.randu(n_rows, n_cols, 15, "bf16", ctx)
+    x, y, d, u, b = (M.to_numpy() for M in (X, Y, D, U, B))
+    f = np.float32
+    Z = fm.Mat(n_rows, n_cols, "f32", ctx)
+    Z.assign(3 * (X % Y) - X / 2 + Y)
+    assert np.array_equal(Z.to_numpy(), (f(3) * (x * y) - x / f(2)) + y)
+    Z.assign(fm.conv_to(U, "f32") * X + fm.conv_to(B, "f32"))
+    assert np.array_equal(Z.to_numpy(), u.astype(f) * x + b.astype(f))
+    W = fm.Mat(n_rows, n_cols, "f64", ctx)
+    W.assign(D * fm.conv_to(X, "f64") - D / 3.0)
+    # X / s is X * (1/s) in the reference (matrix.py:170-176)
+    assert np.array_equal(W.to_numpy(), d * x.astype(np.float64) - (1.0 / 3.0) * d)
+    for _ in range(2):                      # the chunk counter resets between launches
+        Z.assign(X + Y + X + Y + X + Y + X + Y)
+    assert np.array_equal(Z.to_numpy(), ((((((x + y) + x) + y) + x) + y) + x) + y)
