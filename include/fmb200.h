@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FMB200_ABI_VERSION 2
+#define FMB200_ABI_VERSION 3
 
 /* element types (exprtree.ElemType.code) */
 enum {
@@ -61,6 +61,8 @@ enum { FM_MAP_DENSE = 0, FM_MAP_SUBVIEW = 1, FM_MAP_DIAG = 2 };
 #define FM_MAX_SCALARS 32
 #define FM_MAX_REDUCE_OUT 6
 
+/* The *_S opcodes are binary ops whose second operand is slot `arg` (a PUSH
+ * and the op in one dispatch, one stack register less). */
 enum fm_opcode {
   FM_OP_PUSH32 = 0, FM_OP_PUSH64,
   FM_OP_ADD_F, FM_OP_SUB_F, FM_OP_RSUB_F, FM_OP_MUL_F, FM_OP_DIV_F, FM_OP_RDIV_F,
@@ -77,6 +79,9 @@ enum fm_opcode {
   FM_OP_CVT_F_D, FM_OP_CVT_D_F, FM_OP_CVT_F_I, FM_OP_CVT_D_I,
   FM_OP_CVT_I32_F, FM_OP_CVT_U32_F, FM_OP_CVT_I32_D, FM_OP_CVT_U32_D,
   FM_OP_RND_BF_F, FM_OP_CVT_D_BF,
+  FM_OP_ADD_F_S, FM_OP_SUB_F_S, FM_OP_RSUB_F_S, FM_OP_MUL_F_S, FM_OP_DIV_F_S, FM_OP_RDIV_F_S,
+  FM_OP_ADD_D_S, FM_OP_SUB_D_S, FM_OP_RSUB_D_S, FM_OP_MUL_D_S, FM_OP_DIV_D_S, FM_OP_RDIV_D_S,
+  FM_OP_ADD_I_S, FM_OP_SUB_I_S, FM_OP_RSUB_I_S, FM_OP_MUL_I_S,
   FM_OP_COUNT
 };
 

@@ -394,6 +394,21 @@ struct Vm {
   CASE(OP, D) if constexpr (OKB(D)) {                                           \
     VLOOP { uint32_t x = LO(D)[v], y = LO((D) + 1)[v]; LO(D)[v] = (EXPR); }     \
   } break;
+// fused binary ops: the slot operand (yl, yh) is loaded once per
+// instruction before the dispatch (one fetch_slot call site for all of them)
+#define BINS_F(OP, EXPR, D)                                                     \
+  CASE(OP, D) if constexpr (OKD(D)) {                                           \
+    VLOOP { float x = u2f(LO(D)[v]), y = u2f(yl[v]); LO(D)[v] = f2u(EXPR); }    \
+  } break;
+#define BINS_D(OP, EXPR, D)                                                     \
+  CASE(OP, D) if constexpr (WIDE && OKD(D)) {                                   \
+    VLOOP { double x = u2d(LO(D)[v], HI(D)[v]), y = u2d(yl[v], yh[v]);          \
+            d2u(EXPR, LO(D)[v], HI(D)[v]); }                                    \
+  } break;
+#define BINS_I(OP, EXPR, D)                                                     \
+  CASE(OP, D) if constexpr (OKD(D)) {                                           \
+    VLOOP { uint32_t x = LO(D)[v], y = yl[v]; LO(D)[v] = (EXPR); }              \
+  } break;
 #define UN_F(OP, EXPR, D)                                                       \
   CASE(OP, D) if constexpr (OKD(D)) {                                           \
     const float s = u2f((uint32_t)sb); (void)s;                                 \
@@ -429,6 +444,17 @@ struct Vm {
       const int a = ins.arg;
       const uint64_t sb = P.scalars[a & (FM_MAX_SCALARS - 1)];
       (void)sb;
+      uint32_t yl[V], yh[V];
+      if (ins.key >= (FM_OP_ADD_F_S << 3)) {   // slot operand of a fused binary op
+        bool pre = false;
+#pragma unroll
+        for (int j = 0; j < NPF; ++j)
+          if (a == j) {
+            VLOOP { yl[v] = plo[j][v]; yh[v] = phi[j < HP ? j : 0][v]; }
+            pre = true;
+          }
+        if (!pre) fetch_slot<V>(P, a, ch, yl, yh);
+      }
       switch (ins.key) {
         PUSH32(0) PUSH32(1) PUSH32(2) PUSH32(3) PUSH32(4) PUSH32(5) PUSH32(6) PUSH32(7)
         PUSH64(0) PUSH64(1) PUSH64(2) PUSH64(3) PUSH64(4) PUSH64(5) PUSH64(6) PUSH64(7)
@@ -448,6 +474,22 @@ struct Vm {
         ALLD(BIN_I, SUB_I, sub_i(x, y))
         ALLD(BIN_I, RSUB_I, sub_i(y, x))
         ALLD(BIN_I, MUL_I, mul_i(x, y))
+        ALLD(BINS_F, ADD_F_S, add_f(x, y))
+        ALLD(BINS_F, SUB_F_S, sub_f(x, y))
+        ALLD(BINS_F, RSUB_F_S, sub_f(y, x))
+        ALLD(BINS_F, MUL_F_S, mul_f(x, y))
+        ALLD(BINS_F, DIV_F_S, div_f(x, y))
+        ALLD(BINS_F, RDIV_F_S, div_f(y, x))
+        ALLD(BINS_D, ADD_D_S, add_d(x, y))
+        ALLD(BINS_D, SUB_D_S, sub_d(x, y))
+        ALLD(BINS_D, RSUB_D_S, sub_d(y, x))
+        ALLD(BINS_D, MUL_D_S, mul_d(x, y))
+        ALLD(BINS_D, DIV_D_S, div_d(x, y))
+        ALLD(BINS_D, RDIV_D_S, div_d(y, x))
+        ALLD(BINS_I, ADD_I_S, add_i(x, y))
+        ALLD(BINS_I, SUB_I_S, sub_i(x, y))
+        ALLD(BINS_I, RSUB_I_S, sub_i(y, x))
+        ALLD(BINS_I, MUL_I_S, mul_i(x, y))
         ALLD(UN_F, SADD_F, add_f(x, s))
         ALLD(UN_F, SMUL_F, mul_f(s, x))
         ALLD(UN_F, SDIV_F, div_f(s, x))
@@ -509,6 +551,9 @@ struct Vm {
 #undef BIN_F
 #undef BIN_D
 #undef BIN_I
+#undef BINS_F
+#undef BINS_D
+#undef BINS_I
 #undef UN_F
 #undef UN_D
 #undef UN_I

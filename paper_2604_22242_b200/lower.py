@@ -57,6 +57,12 @@ OPCODES = [
     "CVT_F_D", "CVT_D_F", "CVT_F_I", "CVT_D_I",
     "CVT_I32_F", "CVT_U32_F", "CVT_I32_D", "CVT_U32_D",
     "RND_BF_F", "CVT_D_BF",
+    # binary ops whose second operand is a leaf read straight from its slot
+    # (arg = slot): the PUSH + op pair in one VM dispatch and one stack
+    # register less
+    "ADD_F_S", "SUB_F_S", "RSUB_F_S", "MUL_F_S", "DIV_F_S", "RDIV_F_S",
+    "ADD_D_S", "SUB_D_S", "RSUB_D_S", "MUL_D_S", "DIV_D_S", "RDIV_D_S",
+    "ADD_I_S", "SUB_I_S", "RSUB_I_S", "MUL_I_S",
 ]
 OP = {name: i for i, name in enumerate(OPCODES)}
 
@@ -106,8 +112,25 @@ class Program:
         return [f"{OPCODES[op]}@{d} {arg}" for op, d, arg in self.code]
 
 
+def _leaf_under(node: ExprNode):
+    """The leaf a chain of transposes wraps (a slot operand), or None."""
+    while isinstance(node, Transpose):
+        node = node.child
+    return node if isinstance(node, (Leaf, Subview, Diag)) else None
+
+
+def _swap(node: BinaryElem, memo: dict) -> bool:
+    """Evaluate the right child first?  The needier child goes first; on a
+    tie, a lone leaf goes second (it becomes a slot operand)."""
+    a, b = _need(node.left, memo), _need(node.right, memo)
+    if a != b:
+        return b > a
+    return _leaf_under(node.left) is not None and _leaf_under(node.right) is None
+
+
 def _need(node: ExprNode, memo: dict) -> int:
-    """Sethi-Ullman register need."""
+    """Sethi-Ullman register need; a leaf evaluated second is a slot operand
+    of the binary op (no register)."""
     key = id(node)
     if key in memo:
         return memo[key]
@@ -117,7 +140,11 @@ def _need(node: ExprNode, memo: dict) -> int:
         r = _need(node.children()[0], memo)
     elif isinstance(node, BinaryElem):
         a, b = _need(node.left, memo), _need(node.right, memo)
-        r = max(a, b) if a != b else a + 1
+        second = node.left if _swap(node, memo) else node.right
+        if _leaf_under(second) is not None:
+            r = max(a, b)
+        else:
+            r = max(a, b) if a != b else a + 1
     else:
         raise GenerationError(f"{type(node).__name__} reached the lowering; "
                               "fusion barriers must be split during planning")
@@ -215,15 +242,27 @@ class _Lowerer:
         c = _cls(n.etype)
         if c == "D":
             self.prog.wide = True
-        swap = _need(n.right, self.memo) > _need(n.left, self.memo)
+        swap = _swap(n, self.memo)
         first, second = (n.right, n.left) if swap else (n.left, n.right)
         self.lower(first, depth, transposed)
-        self.lower(second, depth + 1, transposed)
         name = {BinaryKind.plus: "ADD", BinaryKind.minus: "SUB",
                 BinaryKind.schur: "MUL", BinaryKind.elem_div: "DIV"}[n.kind]
         if swap and name in ("SUB", "DIV"):
             name = "R" + name
-        self.emit(f"{name}_{c}", depth)
+        leaf = _leaf_under(second)
+        if leaf is not None:
+            # slot operand: the leaf's transposes flip the access like lower() does
+            tr = transposed
+            t = second
+            while isinstance(t, Transpose):
+                tr, t = not tr, t.child
+            s = self.slot(leaf, tr)
+            if leaf.leaf_etype is ElemType.f64:
+                self.prog.wide = True
+            self.emit(f"{name}_{c}_S", depth, s)
+        else:
+            self.lower(second, depth + 1, transposed)
+            self.emit(f"{name}_{c}", depth)
         self.round_bf16(n.etype, depth)
 
     def _unary(self, n: UnaryElem, depth: int, transposed: bool) -> None:

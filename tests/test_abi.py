@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
     for name in header_functions():
         assert hasattr(lib, name), name
     nat = _native.Native()
-    assert nat.lib.fm_abi_version() == 2
+    assert nat.lib.fm_abi_version() == 3
     n = ctypes.c_int(0)
     nat.lib.fm_kernel_count(ctypes.byref(n))
     assert n.value >= 20

@@ -138,9 +138,9 @@ def test_reduce_inside_expression_is_a_barrier():
 def test_c1_program():
     node = ast.plus(ast.scalar_pre_mul(2, ast.schur(L(0), L(1))), L(0))
     p = lower.lower(node)
-    assert p.flat and p.depth == 2 and len(p.slots) == 2
-    assert p.disassemble() == ["PUSH32@0 0", "PUSH32@1 1", "MUL_F@0 0", "SMUL_F@0 0",
-                               "PUSH32@1 0", "ADD_F@0 0"]
+    assert p.flat and p.depth == 1 and len(p.slots) == 2
+    # leaves evaluated second are slot operands of their binary op
+    assert p.disassemble() == ["PUSH32@0 0", "MUL_F_S@0 1", "SMUL_F@0 0", "ADD_F_S@0 0"]
 
 
 def test_sethi_ullman_keeps_deep_trees_shallow():
@@ -148,17 +148,19 @@ def test_sethi_ullman_keeps_deep_trees_shallow():
     while len(leaves) > 1:                       # balanced 64-leaf tree needs 7 registers
         leaves = [ast.minus(leaves[i], leaves[i + 1]) for i in range(0, len(leaves), 2)]
     p = lower.lower(leaves[0])
-    assert p.depth == 7
+    assert p.depth == 6                          # the last level's right leaves are slot operands
     chain = L(0)
-    for i in range(1, 40):                       # left-deep addN needs 2
+    for i in range(1, 40):                       # left-deep addN needs 1 (PUSH, then ADD_F_S ...)
         chain = ast.plus(chain, L(i))
-    assert lower.lower(chain).depth == 2
+    assert lower.lower(chain).depth == 1
 
 
 def test_right_heavy_subtraction_uses_reversed_opcode():
     node = ast.minus(L(0), ast.plus(L(1), L(2)))
     p = lower.lower(node)
-    assert p.disassemble()[-1] == "RSUB_F@0 0"
+    assert p.disassemble()[-1] == "RSUB_F_S@0 0"     # (L1 + L2) first, then L0 as a slot operand
+    node = ast.minus(ast.plus(L(0), L(1)), ast.plus(L(2), L(3)))
+    assert lower.lower(node).disassemble()[-1] == "SUB_F@0 0"
 
 
 def test_views_and_transposes_are_not_flat():
