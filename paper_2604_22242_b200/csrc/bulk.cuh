@@ -383,11 +383,15 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 // dynamically, and kVmWarps consumer warps run the VM out of shared memory
 // (Chunk::bstage: slot j's data at stage + slot.reserved), storing straight
 // to HBM.  Memory parallelism no longer depends on the VM's register use.
-constexpr int kVmWarps = 16;
-constexpr int kVmThreads = (kVmWarps + 1) * 32;
+// consumer warps: 16 for 32-bit VMs (<= 120 registers each); the 64-bit
+// VMs carry twice the stack and keep 8 (<= 224 registers, no spills)
+template <class E> struct VmGeo {
+  static constexpr int kWarps = E::kWide ? 8 : 16;
+  static constexpr int kThreads = (kWarps + 1) * 32;
+};
 
 template <class E>
-__global__ void __launch_bounds__(kVmThreads, 1)
+__global__ void __launch_bounds__(VmGeo<E>::kThreads, 1)
     k_copy_bulk_vm(const __grid_constant__ fm_program P, void *out, int64_t n_elem, unsigned *counters,
                    int chunk_elems, int stages, int stage_bytes) {
   constexpr int V = E::kV;
@@ -398,7 +402,7 @@ __global__ void __launch_bounds__(kVmThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kVmWarps);
+      mbar_init(&empty[s], VmGeo<E>::kWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(kVmThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int64_t nfull = n_elem / chunk_elems;
   unsigned *ctr = counters, *done = counters + 1;
-  if (warp == kVmWarps) {
+  if (warp == VmGeo<E>::kWarps) {
     if ((threadIdx.x & 31) == 0) {
       const uint64_t pol = evict_first_policy();
       int64_t k = 0;
@@ -452,7 +456,7 @@ __global__ void __launch_bounds__(kVmThreads, 1)
       mbar_wait(&full[st], (uint32_t)((k / stages) & 1));
       const int64_t c = cid[st];
       if (c < 0) break;
-      for (int g = ctid; g < groups; g += kVmWarps * 32) {
+      for (int g = ctid; g < groups; g += VmGeo<E>::kWarps * 32) {
         Chunk ch;
         ch.flat = true;
         ch.base = c * chunk_elems + (int64_t)g * V;
@@ -470,7 +474,7 @@ __global__ void __launch_bounds__(kVmThreads, 1)
     }
     // ragged tail (< one chunk): block 0, the VM's global-memory path
     if (blockIdx.x == 0) {
-      for (int64_t e0 = nfull * chunk_elems + (int64_t)ctid * V; e0 < n_elem; e0 += (int64_t)kVmWarps * 32 * V) {
+      for (int64_t e0 = nfull * chunk_elems + (int64_t)ctid * V; e0 < n_elem; e0 += (int64_t)VmGeo<E>::kWarps * 32 * V) {
         Chunk ch;
         ch.base = e0;
         ch.cnt = (int)min((int64_t)V, n_elem - e0);
@@ -490,6 +494,182 @@ __global__ void __launch_bounds__(kVmThreads, 1)
       *ctr = 0u;
       *done = 0u;
     }
+  }
+}
+
+// Full reduction on the register VM over bulk-staged chunks (accu of a flat
+// program with no template): the same producer / consumer ring as
+// k_copy_bulk_vm; a static head of chunks round-robin summed per CTA, the
+// rest claimed dynamically with one partial slot each (fixed summation order
+// within a chunk), combined in chunk order by the last CTA -- deterministic
+// for a given grid, like k_accu_bulk.  Floats accumulate in f64, integers
+// wrap in 32 bits (codegen.py:47-49).
+template <class E>
+__global__ void __launch_bounds__(VmGeo<E>::kThreads, 1)
+    k_accu_bulk_vm(const __grid_constant__ fm_program P, void *out, int64_t n_elem, int finalize, double *part_d,
+                   uint32_t *part_u, unsigned *counters, int chunk_elems, int stages, int stage_bytes) {
+  constexpr int V = E::kV;
+  constexpr int NW = VmGeo<E>::kWarps;
+  extern __shared__ __align__(128) unsigned char vsm[];
+  uint64_t *full = (uint64_t *)(vsm + (size_t)stages * stage_bytes);
+  uint64_t *empty = full + stages;
+  int64_t *cid = (int64_t *)(empty + stages);
+  __shared__ double wd[2][NW];
+  __shared__ uint32_t wu[2][NW];
+  __shared__ double smd[NW + 1];
+  __shared__ uint32_t smu[NW + 1];
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int indep = P.reserved & 1;
+  pdl_enter(indep);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rt = P.result_etype;
+  const bool fl = is_float_etype(rt);
+  const int64_t nfull = n_elem / chunk_elems;
+  const int64_t nstat = nfull * 3 / 4 / gridDim.x;
+  const int64_t dbase = nstat * gridDim.x;
+  double *part_c = part_d + gridDim.x;       // one slot per dynamic chunk
+  uint32_t *part_cu = part_u + gridDim.x;
+  unsigned *done = counters, *ctr = counters + 1;
+  double accd = 0.0;
+  uint32_t accu = 0;
+  if (warp == NW) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int64_t k = 0;
+      auto stage_for = [&](int64_t kk) {
+        const int st = (int)(kk % stages);
+        if (kk >= stages) mbar_wait(&empty[st], (uint32_t)(((kk / stages) & 1) ^ 1));
+        return st;
+      };
+      auto issue = [&](int64_t c) {
+        const int st = stage_for(k++);
+        cid[st] = c;
+        mbar_expect_tx(&full[st], (uint32_t)stage_bytes);
+        for (int j = 0; j < P.n_slots; ++j) {
+          const fm_slot &sl = P.slots[j];
+          const int w = sl.etype == FM_F64 ? 8 : (sl.etype == FM_BF16 ? 2 : 4);
+          bulk_g2s(vsm + (size_t)st * stage_bytes + sl.reserved, (const unsigned char *)sl.ptr + c * chunk_elems * w,
+                   (uint32_t)chunk_elems * w, &full[st], pol);
+        }
+      };
+      for (int64_t j = 0; j < nstat; ++j) issue(blockIdx.x + j * gridDim.x);
+      int64_t c = dbase + atomicAdd(ctr, 1u);
+      while (c < nfull) {
+        const int64_t next = dbase + atomicAdd(ctr, 1u);
+        issue(c);
+        c = next;
+      }
+      const int st = stage_for(k);
+      cid[st] = -1;
+      mbar_arrive(&full[st]);
+    }
+  } else {
+    const int ctid = threadIdx.x;
+    const int groups = chunk_elems / V;
+    int par = 0;
+    for (int64_t k = 0;; ++k) {
+      const int st = (int)(k % stages);
+      mbar_wait(&full[st], (uint32_t)((k / stages) & 1));
+      const int64_t c = cid[st];
+      if (c < 0) break;
+      double cd = 0.0;
+      uint32_t cu = 0;
+      for (int g = ctid; g < groups; g += NW * 32) {
+        Chunk ch;
+        ch.flat = true;
+        ch.base = c * chunk_elems + (int64_t)g * V;
+        ch.cnt = V;
+        ch.row0 = 0;
+        ch.col = 0;
+        ch.bstage = vsm + (size_t)st * stage_bytes;
+        ch.boff = g * V;
+        uint32_t lo[V], hi[V];
+        E::eval(P, ch, lo, hi);
+        if (fl) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) cd = add_d(cd, as_double(rt, lo[v], hi[v]));
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) cu += lo[v];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (c < dbase) {
+        accd = add_d(accd, cd);
+        accu += cu;
+      } else {
+        // dynamic chunk: its own partial, reduced in a fixed order
+        cd = warp_sum_d(cd);
+        cu = warp_sum_u(cu);
+        if (lane == 0) { wd[par][warp] = cd; wu[par][warp] = cu; }
+        asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");   // consumer warps only
+        if (ctid == 0) {
+          double t = 0.0;
+          uint32_t tu = 0;
+          for (int w = 0; w < NW; ++w) { t = add_d(t, wd[par][w]); tu += wu[par][w]; }
+          part_c[c - dbase] = t;
+          part_cu[c - dbase] = tu;
+        }
+        par ^= 1;
+      }
+    }
+    if (blockIdx.x == gridDim.x - 1) {   // ragged tail (< one chunk): the VM's global-memory path
+      for (int64_t e0 = nfull * chunk_elems + (int64_t)ctid * V; e0 < n_elem; e0 += (int64_t)NW * 32 * V) {
+        Chunk ch;
+        ch.base = e0;
+        ch.cnt = (int)min((int64_t)V, n_elem - e0);
+        ch.row0 = 0; ch.col = 0; ch.flat = true;
+        uint32_t lo[V], hi[V];
+        E::eval(P, ch, lo, hi);
+        for (int v = 0; v < ch.cnt; ++v) {
+          if (fl) accd = add_d(accd, as_double(rt, lo[v], hi[v]));
+          else accu += lo[v];
+        }
+      }
+    }
+  }
+  // per-CTA partial (the producer warp contributes 0)
+  accd = warp_sum_d(accd);
+  accu = warp_sum_u(accu);
+  __syncthreads();
+  if (lane == 0) { smd[warp] = accd; smu[warp] = accu; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    uint32_t bu = 0;
+    for (int w = 0; w <= NW; ++w) { b = add_d(b, smd[w]); bu += smu[w]; }
+    part_d[blockIdx.x] = b;
+    part_u[blockIdx.x] = bu;
+    __threadfence();
+    last = (atomicAdd(done, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) pdl_exit(indep);
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    const int64_t ndyn = nfull - dbase;
+    double a = 0.0;
+    uint32_t au = 0;
+    for (int i = 0; i < (int)gridDim.x; ++i) { a = add_d(a, __ldcg(part_d + i)); au += __ldcg(part_u + i); }
+    for (int64_t i = 0; i < ndyn; ++i) { a = add_d(a, __ldcg(part_c + i)); au += __ldcg(part_cu + i); }
+    if (fl) {
+      if (finalize == FM_FINAL_SQRT) a = sqrt_d(a);
+      *(double *)out = a;
+    } else {
+      *(uint32_t *)out = au;
+    }
+    *done = 0u;
+    *ctr = 0u;
   }
 }
 

@@ -152,9 +152,53 @@ int run_copy_bulk_vm(const fm_program &P0, void *out, int64_t n_elem, cudaStream
   Scratch sc;
   if (int st = get_scratch((void *)s, 64, &sc, cl.slot)) return st;
   const int64_t grid = std::min<int64_t>(n_elem / chunk, sm_count());
-  FM_CHECK(launch_pdl(bulk::k_copy_bulk_vm<typename NoPrefetch<E>::type>, dim3((unsigned)grid), dim3(bulk::kVmThreads),
-                      smem, s, cl.P, out, n_elem, sc.counters, chunk, stages, stage_bytes));
+  using EV = typename NoPrefetch<E>::type;
+  FM_CHECK(launch_pdl(bulk::k_copy_bulk_vm<EV>, dim3((unsigned)grid), dim3(bulk::VmGeo<EV>::kThreads), smem, s, cl.P,
+                      out, n_elem, sc.counters, chunk, stages, stage_bytes));
   FM_CHECK_LAUNCH("fused copy kernel (VM, bulk-staged)");
+  handled = true;
+  return 0;
+}
+
+// Full reduction of a flat program on the VM over bulk-staged chunks
+// (bulk.cuh k_accu_bulk_vm); eligibility as run_copy_bulk_vm.
+template <class E>
+int run_accu_bulk_vm(const fm_program &P0, void *out, int64_t n_elem, int finalize, cudaStream_t s, bool &handled) {
+  handled = false;
+  if (!P0.flat || P0.n_slots < 1 || P0.n_slots > 8) return 0;
+  fm_program P = P0;
+  int bytes_per_elem = 0;
+  for (int j = 0; j < P.n_slots; ++j) {
+    if (((uintptr_t)P.slots[j].ptr) & 15) return 0;
+    bytes_per_elem += etype_bytes(P.slots[j].etype);
+  }
+  const int chunk = (200 * 1024 / 4 / bytes_per_elem) / 256 * 256;
+  if (chunk < 256 || n_elem < (int64_t)chunk * sm_count()) return 0;
+  int off = 0;
+  for (int j = 0; j < P.n_slots; ++j) {
+    P.slots[j].reserved = off;
+    off += chunk * etype_bytes(P.slots[j].etype);
+  }
+  const int stage_bytes = off, stages = 4;
+  const size_t smem = (size_t)stages * stage_bytes + (size_t)stages * 24 + 64;
+  using EV = typename NoPrefetch<E>::type;
+  static bool attr = false;
+  if (!attr) {
+    FM_CHECK(cudaFuncSetAttribute(bulk::k_accu_bulk_vm<EV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    attr = true;
+  }
+  const int64_t grid = std::min<int64_t>(n_elem / chunk, sm_count());
+  const int64_t nfull = n_elem / chunk;
+  const int64_t ndyn = nfull - (nfull * 3 / 4 / grid) * grid;
+  const Classified cl = classify(s, P, n_elem, 1, writes_of(out, 8));
+  Scratch sc;
+  if (int st = get_scratch((void *)s, (size_t)(grid + ndyn) * (sizeof(double) + sizeof(uint32_t)) + 64, &sc, cl.slot))
+    return st;
+  double *pd = (double *)sc.payload;
+  uint32_t *pu = (uint32_t *)(pd + grid + ndyn);
+  FM_CHECK(launch_pdl(bulk::k_accu_bulk_vm<EV>, dim3((unsigned)grid), dim3(bulk::VmGeo<EV>::kThreads), smem, s, cl.P, out,
+                      n_elem, finalize, pd, pu, sc.counters, chunk, stages, stage_bytes));
+  FM_CHECK_LAUNCH("fused accu kernel (VM, bulk-staged)");
   handled = true;
   return 0;
 }
@@ -284,6 +328,11 @@ template <class E>
 int run_accu(const fm_program &P, void *out, int64_t n_rows, int64_t n_cols, int finalize,
              cudaStream_t s) {
   constexpr int V = E::kV;
+  if constexpr (E::kIsVm) {
+    bool handled = false;
+    if (int st = run_accu_bulk_vm<E>(P, out, n_rows * n_cols, finalize, s, handled)) return st;
+    if (handled) return 0;
+  }
   if constexpr (E::kFast) {
     if constexpr (bulk::Geometry<E>::kOk) {
       const int64_t n = n_rows * n_cols;

@@ -38,6 +38,33 @@ cases = [("c1 2*(X%Y)+X", lambda X, Y: 2 * (X % Y) + X, 2),
          ("add8", lambda *m: m[0] + m[1] + m[2] + m[3] + m[4] + m[5] + m[6] + m[7], 8),
          ("sigmoid", lambda X: 1 / (1 + fm.exp(-X)), 1),
          ("c3", lambda X, Y: fm.exp(-fm.square(X - Y) / 2) + 0.5 * fm.abs(X), 2)]
+def accu_gbs(use_templates, build, nin, n=8192, reps=20):
+    be = fm.B200Backend(use_templates=use_templates)
+    ctx = fm.Context(be)
+    ms = [fm.randu(n * n, 1, 40 + i, "f32", ctx) for i in range(nin)]
+    R = fm.Mat(1, 1, "f64", ctx)
+    e = build(*ms)
+    for _ in range(3):
+        fm.accu_async(e, R)
+    g = fm.capture(lambda: [fm.accu_async(e, R) for _ in range(reps)], ctx)
+    a, b = ctypes.c_void_p(), ctypes.c_void_p()
+    nat.call("fm_event_create", ctypes.byref(a))
+    nat.call("fm_event_create", ctypes.byref(b))
+    g.replay()
+    ctx.sync()
+    nat.call("fm_event_record", a.value, be.stream)
+    g.replay()
+    nat.call("fm_event_record", b.value, be.stream)
+    f = ctypes.c_float()
+    nat.call("fm_event_elapsed_ms", a.value, b.value, ctypes.byref(f))
+    return nin * 4 * n * n / (f.value / reps * 1e-3) / 1e9
+
+
+for name, build, nin in [("accu dot", lambda X, Y: X % Y, 2), ("accu 3x-y", lambda X, Y: 3 * X - Y, 2)]:
+    t = accu_gbs(True, build, nin)
+    v = accu_gbs(False, build, nin)
+    print(f"{name:14s} template {t:8.1f} GB/s   VM {v:8.1f} GB/s   VM/template {v / t:.2f}", flush=True)
+
 for name, build, nin in cases:
     t = gbs(True, build, nin)
     v = gbs(False, build, nin)

@@ -203,3 +203,28 @@ def test_vm_bulk_staged_copies(vm_ctx, n_rows, n_cols):
     for _ in range(2):                      # the chunk counter resets between launches
         Z.assign(X + Y + X + Y + X + Y + X + Y)
     assert np.array_equal(Z.to_numpy(), ((((((x + y) + x) + y) + x) + y) + x) + y)
+
+
+@pytest.mark.parametrize("n", [4_000_000, 5_000_011])
+def test_vm_bulk_staged_accu(vm_ctx, n):
+    """Full reductions of flat programs on the VM over bulk-staged chunks
+    (bulk.cuh k_accu_bulk_vm): f64 accumulation within 1e-12 of the exactly
+    rounded sum, wrapping u32 sums exact, deterministic run to run."""
+    ctx = vm_ctx
+    x = fm.randu(n, 1, 21, "f32", ctx)
+    y = fm.randu(n, 1, 22, "f32", ctx)
+    d = fm.randu(n, 1, 23, "f64", ctx)
+    u = fm.randi(n, 1, 1000, 24, "u32", ctx)
+    xv, yv, dv, uv = (M.to_numpy().ravel() for M in (x, y, d, u))
+    f = np.float32
+    got = fm.accu(3 * (x % y) - x)
+    want = orc.accu(f(3) * (xv * yv) - xv, fm.ElemType.f32)
+    assert abs(got - want) <= 1e-12 * abs(want)
+    assert fm.accu(3 * (x % y) - x) == got                       # deterministic
+    got = fm.accu(d * fm.conv_to(x, "f64") + d)
+    want = orc.accu(dv * xv.astype(np.float64) + dv, fm.ElemType.f64)
+    assert abs(got - want) <= 1e-12 * abs(want)
+    assert fm.accu(u * 3 + u) == int((uv.astype(np.uint64) * 4).sum() & 0xFFFFFFFF)
+    got = fm.norm(x - 2 * y)
+    want = float(np.sqrt(orc.accu(((xv - f(2) * yv) ** 2).astype(f), fm.ElemType.f32)))
+    assert abs(got - want) <= 1e-12 * want
