@@ -60,8 +60,12 @@ __device__ __forceinline__ double sqrt_d(double a) { return __dsqrt_rn(a); }
 // chain stays memory-bound (C3 is one exp per element), and short: 10 FP64
 // operations per element (the previous table-free degree-11 form took 16 and
 // kept C3 issue-bound, profiles/r01/ncu_c3_copy.txt):
-//   n = rint(x * 64/ln2)   (magic-constant rounding inside one DFMA),
-//   r = x - n*ln2/64       (Cody-Waite hi/lo, exact hi product), |r| <= ln2/128,
+//   n = rint(x * 64/ln2)   (magic-constant rounding inside one DFMA; the
+//                          multiplier kept to 20 bits so it is an instruction
+//                          immediate -- n may differ by one at a boundary,
+//                          |r| stays <= ln2/128 * (1 + 2^-13)),
+//   r = x - n*ln2/64       (Cody-Waite: a 21-bit hi, so n*hi and x - n*hi are
+//                          exact, and a full f64 lo), |r| <= ln2/128,
 //   exp(r) - 1             degree-5 Taylor polynomial (truncation 2^-54.6),
 //   2^(j/64)               64-entry table of correctly rounded f64 values
 //                          (j = n mod 64; read through L1, 512 bytes),
@@ -93,12 +97,12 @@ __device__ __forceinline__ float exp_f(float a) {
   const float c = fminf(fmaxf(a, -104.0f), 89.0f);
   const double x = (double)c;
   const double kMagic = 0x1.8p52;
-  const double t = fma(x, 0x1.71547652b82fep+6, kMagic);   // rint(x*64/ln2) + 1.5*2^52
+  const double t = fma(x, 0x1.71547p+6, kMagic);          // rint(x*64/ln2) + 1.5*2^52 (20-bit multiplier)
   const double n = __dsub_rn(t, kMagic);
   const int ni = __double2loint(t);
-  double r = fma(-n, 0x1.62e42fee00000p-7, x);             // ln2/64 hi (exact n*hi)
-  r = fma(-n, 0x1.a39ef35793c76p-39, r);                   // ln2/64 lo
-  double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  double r = fma(-n, 0x1.62e43p-7, x);                     // ln2/64 hi, 21 bits (n*hi and x - n*hi exact)
+  r = fma(n, 0x1.05c610ca86c39p-35, r);                    // - ln2/64 lo (hi - ln2/64)
+  double q = fma(r, 0x1.11111p-7, 0x1.5555555555555p-5);   // 1/120 (20 bits: error r^5 2^-21 < 2^-60), 1/24
   q = fma(q, r, 1.0 / 6.0);
   q = fma(q, r, 0.5);
   q = fma(q, r, 1.0);
@@ -240,12 +244,12 @@ __device__ __forceinline__ float tanh_f(float a) {
   const float ax = fabsf(a);
   const double y = 2.0 * (double)fminf(ax, 9.5f);
   const double kMagic = 0x1.8p52;
-  const double t = fma(y, 0x1.71547652b82fep+6, kMagic);   // rint(y*64/ln2) + 1.5*2^52
+  const double t = fma(y, 0x1.71547p+6, kMagic);          // rint(y*64/ln2) + 1.5*2^52 (20-bit multiplier)
   const double n = __dsub_rn(t, kMagic);
   const int ni = __double2loint(t);
-  double r = fma(-n, 0x1.62e42fee00000p-7, y);
-  r = fma(-n, 0x1.a39ef35793c76p-39, r);
-  double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  double r = fma(-n, 0x1.62e43p-7, y);
+  r = fma(n, 0x1.05c610ca86c39p-35, r);
+  double q = fma(r, 0x1.11111p-7, 0x1.5555555555555p-5);
   q = fma(q, r, 1.0 / 6.0);
   q = fma(q, r, 0.5);
   q = fma(q, r, 1.0);
