@@ -576,3 +576,25 @@ def test_back_to_back_reductions_share_no_scratch(ctx):
         ctx.sync()
         assert list(R.to_numpy().ravel()) == pytest.approx(want, rel=1e-13)
     g.close()
+
+
+def test_dependent_launch_two_back(ctx):
+    """A launch that reads what the launch TWO back wrote, with an
+    independent launch in between (the window holds both): it must wait for
+    both.  Large enough that the middle launch's overlap is real."""
+    n = 1 << 24
+    X = fm.randu(n, 1, 501, "f32", ctx)
+    Y = fm.randu(n, 1, 502, "f32", ctx)
+    T, U, W = (fm.Mat(n, 1, "f32", ctx) for _ in range(3))
+    x, y = X.to_numpy(), Y.to_numpy()
+    for rep in range(4):
+        T.assign(X * 3.0 + rep)                 # A
+        U.assign(Y + 1.0)                       # B: independent of A
+        W.assign(T - U)                         # C: reads A's and B's outputs
+        s = fm.accu_async(W)                    # reads C's output
+        ctx.sync()
+        f = np.float32
+        t = x * f(3.0) + f(rep)
+        want = t - (y + f(1.0))
+        assert np.array_equal(W.to_numpy(), want)
+        assert s.result() == pytest.approx(orc.accu(want, fm.ElemType.f32), rel=1e-12)
