@@ -228,3 +228,42 @@ def test_vm_bulk_staged_accu(vm_ctx, n):
     got = fm.norm(x - 2 * y)
     want = float(np.sqrt(orc.accu(((xv - f(2) * yv) ** 2).astype(f), fm.ElemType.f32)))
     assert abs(got - want) <= 1e-12 * want
+
+
+# ---- randomized trees at bulk scale: the VM's bulk-staged kernels and the
+# tile-pair kernel see every operator on >= a wave of chunks, against the
+# oracle's per-node rounding (exact operators only: 0 ulp)
+
+def _rand_expr(rng, leaves, depth, square):
+    if depth == 0 or rng.random() < 0.25:
+        m = leaves[rng.integers(len(leaves))]
+        return m.t() if square and rng.random() < 0.3 else m
+    k = rng.integers(8)
+    a = _rand_expr(rng, leaves, depth - 1, square)
+    if k < 4:
+        b = _rand_expr(rng, leaves, depth - 1, square)
+        return [a + b, a - b, a % b, a / (b + 2.0)][k]
+    s = float(rng.integers(1, 9)) / 4.0
+    return [s * a, a + s, -a, fm.abs(a)][k - 4]
+
+
+@pytest.mark.parametrize("etype", ["f32", "f64"])
+@pytest.mark.parametrize("square", [False, True])
+def test_random_trees_at_bulk_scale(vm_ctx, gpu_ctx, etype, square):
+    rng = np.random.default_rng(7 if square else 8)
+    for ctx in (vm_ctx, gpu_ctx):
+        shape = (1024, 1024) if square else (2048, 640)
+        leaves = [fm.randu(*shape, 600 + i, etype, ctx) for i in range(4)]
+        env = {m.mat_id: m.to_numpy() for m in leaves}
+        Z = fm.Mat(*shape, etype, ctx)
+        for t in range(12):
+            e = _rand_expr(rng, leaves, 4, square)
+            if not hasattr(e, "node"):
+                e = e + 0.0
+            Z.assign(e)
+            want = orc.materialize(e.node, env)
+            assert orc.max_ulp(Z.to_numpy(), want) == 0, (etype, square, t, str(e.node)[:200])
+            if not square:                       # and the full reduction of the same tree
+                exact = orc.accu(want, e.node.etype)
+                scale = orc.accu(np.abs(want), e.node.etype)
+                assert abs(fm.accu(e) - exact) <= 1e-12 * scale, (etype, t)
