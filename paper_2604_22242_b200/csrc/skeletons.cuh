@@ -120,8 +120,10 @@ constexpr int kCopyDepth() {
   // TB/s at depth 2; single-input heavy chains (sigmoid, swish, gelu) lose
   // 2-4 % to the extra registers
   if constexpr (E::kFast) return (FM_COPY_DEPTH2_HEAVY && E::kHeavy && E::kNin >= 2) ? 2 : 1;
-  else return 1;
+  else return 0;   // wide tiles: no tile prefetched ahead
 }
+template <class E, bool VM = E::kIsVm> struct WideTile { static constexpr bool v = false; };
+template <class E> struct WideTile<E, false> { static constexpr bool v = E::kWideTile; };
 
 template <class E>
 __global__ void __launch_bounds__(kThreads, E::kMinBlocks) k_copy(const __grid_constant__ fm_program P, void *out,
@@ -132,14 +134,20 @@ __global__ void __launch_bounds__(kThreads, E::kMinBlocks) k_copy(const __grid_c
   const int64_t n_elem = n_rows * n_cols;
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if constexpr (E::kFast) {
+  if constexpr (E::kFast || WideTile<E>::v) {
     if (E::fast_ok(P, out)) {
       constexpr int kTile = E::kTile;
       const int lane = threadIdx.x & 31;
       const int64_t nwarp = stride >> 5;
       const int64_t ntile = n_elem / kTile;
       int64_t t = c >> 5;
-      if constexpr (kCopyDepth<E>() == 2) {
+      if constexpr (kCopyDepth<E>() == 0) {
+        for (; t < ntile; t += nwarp) {
+          typename E::Buf b;
+          E::load_tile(P, t * kTile, lane, b);
+          E::copy_tile(P, out, t * kTile, lane, b);
+        }
+      } else if constexpr (kCopyDepth<E>() == 2) {
         // long per-element math: two tiles in flight per warp
         typename E::Buf b0, b1;
         if (t < ntile) E::load_tile(P, t * kTile, lane, b0);

@@ -132,10 +132,15 @@ struct TEval {
   // warp-tile fast path (a second tile of every input in flight) up to 8
   // inputs; wider chains (add-N) load all inputs of a chunk at once instead
   static constexpr bool kFast = NIN <= 8;
+  // the wide add-N chains (9..32 inputs) take the copy skeleton's warp tiles
+  // too, one tile per warp at a time (NIN x V words per lane already keep
+  // 128-512 B per lane in flight); before, they ran the general chunk path at
+  // ~200 instructions per element (profiles: add32N issue 24 %, LDL/STL)
+  static constexpr bool kWideTile = NIN > 8 && NIN <= 32;
   static constexpr bool kIsVm = false;
   // the widest chains (add-N, N > 16) hold NIN x V loaded words per thread:
   // ask for two resident blocks so they keep 16 warps per SM
-  static constexpr int kMinBlocks = NIN > 16 ? 2 : 1;
+  static constexpr int kMinBlocks = 1;
   static constexpr bool kWide = sizeof(T) == 8;
   static constexpr bool kHeavy = Heavy<Expr>::v;
   static constexpr bool kRegTiles = RegTiles<Expr>::v;
