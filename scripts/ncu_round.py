@@ -24,6 +24,7 @@ CAPS = {
     "ncu_c5f32_gemm": (r"k_gemm_bf16_pair", "c5f32", 0),
     "ncu_suite_expr1": (r"k_copy_pair<.*SMul<\(int\)1, .*float", "suite", 0),
     "ncu_suite_expr2": (r"k_copy_pair<.*Log<.*float", "suite", 0),
+    "ncu_suite_add32": (r"k_copy<.*In<\(int\)31>", "suite", 0),
 }
 
 
