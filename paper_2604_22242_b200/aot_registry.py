@@ -59,6 +59,25 @@ def hot_expressions() -> list[tuple[str, ast.ExprNode]]:
             ast.scalar_pre_mul(0.5, X),
             ast.scalar_add(ast.tanh(ast.scalar_pre_mul(coeff, ast.plus(
                 X, ast.scalar_pre_mul(0.044715, ast.pow_int(X, 3))))), 1))))
+    # common elementwise forms users write beyond the configs and the suite
+    # (BLAS-1 style updates, differences, quotients, unary maps): templates
+    # run them at the streaming rate instead of on the register VM
+    for ety in (ElemType.f32, ElemType.f64):
+        t = ety.value
+        X, Y, Z = _m(0, ety), _m(1, ety), _m(2, ety)
+        out.append((f"axpy_{t}", ast.plus(ast.scalar_pre_mul(2.0, X), Y)))
+        out.append((f"axpby_{t}", ast.plus(ast.scalar_pre_mul(2.0, X), ast.scalar_pre_mul(3.0, Y))))
+        out.append((f"sub_{t}", ast.minus(X, Y)))
+        out.append((f"div_{t}", ast.elem_div(X, Y)))
+        out.append((f"scale_{t}", ast.scalar_pre_mul(2.0, X)))
+        out.append((f"shift_{t}", ast.scalar_add(X, 1.0)))
+        out.append((f"muladd_{t}", ast.plus(ast.schur(X, Y), Z)))
+        out.append((f"absdiff_{t}", ast.abs_(ast.minus(X, Y))))
+        out.append((f"square_{t}", ast.square(X)))
+        out.append((f"sqrt_{t}", ast.sqrt(X)))
+        out.append((f"exp_{t}", ast.exp(X)))
+        out.append((f"log_{t}", ast.log(X)))
+        out.append((f"neg_{t}", ast.neg(X)))
     # paper suite members with views / transposes (bench.py:119-147): leaves
     # read through index maps; copies run on the tiled staged skeleton
     _B = MatShape(8, 8)

@@ -34,6 +34,9 @@ def gbs(use_templates, build, nin, n=8192, reps=20):
 
 
 cases = [("c1 2*(X%Y)+X", lambda X, Y: 2 * (X % Y) + X, 2),
+         ("axpby", lambda X, Y: 1.5 * X + 0.25 * Y, 2),
+         ("muladd", lambda X, Y, Z: X % Y + Z, 3),
+         ("sqrt", lambda X: fm.sqrt(X), 1),
          ("add4", lambda A, B, C, D: A + B + C + D, 4),
          ("add8", lambda *m: m[0] + m[1] + m[2] + m[3] + m[4] + m[5] + m[6] + m[7], 8),
          ("sigmoid", lambda X: 1 / (1 + fm.exp(-X)), 1),
