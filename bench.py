@@ -1003,14 +1003,27 @@ def measure(run: Run, cfg: Config, steps: int, warmup: int, with_cpu: bool, with
     # region replays the same kernels on the same buffers with no host planning.
     # Events only at step boundaries there; per-kernel times come from a second,
     # instrumented pass (an event between two kernels costs ~6 us).
-    g_step = g_instr = None
+    # With an L2 flush between steps the flush is captured into the step's
+    # graph, right before the start event: the device runs flush -> step with
+    # no host gap (a large graph's launch can outlast the flush, and the first
+    # kernel after an idle GPU runs ~40 us slow, scripts/first_after_flush.py).
+    sev = Events(nat, backend.stream, 2 * steps)
+
+    def step_timed(s):
+        flush()
+        sev.record(2 * s)
+        step_plain()
+        sev.record(2 * s + 1)
+
+    g_step = g_instr = g_timed = None
     if use_graph:
         g_step = fm.capture(step_plain, run.ctx)
-        g_instr = [fm.capture(lambda s=s: step_instrumented(s), run.ctx) for s in range(steps)]
+        if flush_h is not None:
+            g_timed = [fm.capture(lambda s=s: step_timed(s), run.ctx) for s in range(steps)]
+        g_instr = [fm.capture(lambda s=s: (flush(), step_instrumented(s)), run.ctx) for s in range(steps)]
         g_step.replay()
         run.sync()
         p.barrier()
-    sev = Events(nat, backend.stream, 2 * steps)
     sampler = ClockSampler(p.device).start()
     time.sleep(0.25)
     run.sync()
@@ -1018,6 +1031,9 @@ def measure(run: Run, cfg: Config, steps: int, warmup: int, with_cpu: bool, with
     c0 = nat.lib.fm_launch_counter()
     t_wall0 = time.perf_counter()
     for s in range(steps):
+        if g_timed is not None:
+            g_timed[s].replay()
+            continue
         flush()
         sev.record(2 * s)
         if g_step is not None:
@@ -1035,14 +1051,14 @@ def measure(run: Run, cfg: Config, steps: int, warmup: int, with_cpu: bool, with
     run.sync()
     p.barrier()
     for s in range(steps):
-        flush()
         if g_instr is not None:
             g_instr[s].replay()
         else:
+            flush()
             step_instrumented(s)
     run.sync()
     per_kernel = [[ev.ms(s * (nk + 1) + i, s * (nk + 1) + i + 1) for s in range(steps)] for i in range(nk)]
-    for g in [g_step] + (g_instr or []):
+    for g in [g_step] + (g_instr or []) + (g_timed or []):
         if g is not None:
             g.close()
     ev.close()
