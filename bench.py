@@ -64,8 +64,10 @@ METRIC = "fused-expression effective HBM GB/s (% of 8 TB/s) and elements/s at 1/
 SPEC_HBM_GBS = 8000.0
 FALLBACK_HBM_GBS = 6650.0
 FALLBACK_BF16_TFLOPS = 1590.0
-TIMING_NOTE = ("achieved = algorithmic work / mean launch duration from CUDA events between the kernels "
-               "(a second, instrumented pass of the timed steps; each event adds ~6 us); "
+TIMING_NOTE = ("achieved = algorithmic work / mean launch duration of the dominant kernel (all its launches "
+               "in the step) from CUDA events between the kernels (a second, instrumented pass of the timed "
+               "steps; each event adds ~6 us); when every launch of the step is that kernel, the events at "
+               "the timed steps' boundaries give the duration directly (no events between launches); "
                "achieved_in_timed_steps = the kernel's share of the instrumented step applied to the "
                "event-free timed step")
 
@@ -1074,23 +1076,40 @@ def measure(run: Run, cfg: Config, steps: int, warmup: int, with_cpu: bool, with
     peaks = measured_peaks()
     means = [statistics.fmean(v) for v in per_kernel]
     share = [sum(v) for v in per_kernel]
-    dom = int(np.argmax([s if w else -1 for s, w in zip(share, kwork)]))
-    achieved = kwork[dom] / (means[dom] * 1e-3) / scale
-    in_step = kwork[dom] / (statistics.fmean(steps_ms) * share[dom] / sum(share) * 1e-3) / scale
-    common = {"kernel": labels[dom], "achieved": round(achieved, 1), "traffic": ncu_traffic(labels[dom]),
-              "mean_launch_us": round(means[dom] * 1e3, 2), "achieved_in_timed_steps": round(in_step, 1),
+    # launches of one kernel ("c1_copy_f32[0..5]") form a family: the
+    # dominant kernel is the family with the largest share of the step
+    fam = [l.split("[")[0] for l in labels]
+    fams = sorted({f for f, w in zip(fam, kwork) if w})
+    fshare = {f: sum(s for s, g in zip(share, fam) if g == f) for f in fams}
+    fwork = {f: sum(w for w, g in zip(kwork, fam) if g == f) for f in fams}
+    fcount = {f: sum(1 for g in fam if g == f) for f in fams}
+    dfam = max(fams, key=lambda f: fshare[f])
+    step_mean = statistics.fmean(steps_ms)
+    if len(set(fam)) == 1:
+        # the whole step is this kernel: its launches' mean duration is the
+        # event-timed step over the launch count
+        mean_launch = step_mean / fcount[dfam]
+    else:
+        mean_launch = fshare[dfam] / (steps * fcount[dfam])
+    work_launch = fwork[dfam] / fcount[dfam]
+    achieved = work_launch / (mean_launch * 1e-3) / scale
+    in_step = fwork[dfam] / (step_mean * fshare[dfam] / sum(share) * 1e-3) / scale
+    dom = fam.index(dfam)
+    common = {"kernel": dfam, "launches_per_step": fcount[dfam], "achieved": round(achieved, 1),
+              "traffic": ncu_traffic(labels[dom]),
+              "mean_launch_us": round(mean_launch * 1e3, 2), "achieved_in_timed_steps": round(in_step, 1),
               "timing": TIMING_NOTE}
     if tensor:
         peak = peaks["bf16_tflops"]
         roofline = {"bound": "tensor", "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                     "frac_of_sustained": round(achieved / peaks["bf16_tflops_sustained"], 4),
                     "frac_of_2250_spec": round(achieved / 2250.0, 4),
-                    "peak_source": peaks["source"] + " bf16 burst", "algorithmic_flops_per_launch": kwork[dom],
+                    "peak_source": peaks["source"] + " bf16 burst", "algorithmic_flops_per_launch": work_launch,
                     **common}
     else:
         roofline = {"bound": "hbm", "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": round(achieved / peaks["hbm_gbs"], 4), "frac_of_8TBs": round(achieved / SPEC_HBM_GBS, 4),
-                    "peak_source": peaks["source"], "algorithmic_bytes_per_launch": kwork[dom], **common,
+                    "peak_source": peaks["source"], "algorithmic_bytes_per_launch": work_launch, **common,
                     "per_kernel_gbs": {lab: round(b / (m * 1e-3) / 1e9, 1) for lab, b, m in zip(labels, kwork, means)
                                        if b}}
     out = {"metric": cfg.metric, "value": round(value, 2), "unit": cfg.unit, "n_gpus": run.world,
