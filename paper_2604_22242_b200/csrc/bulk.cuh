@@ -72,25 +72,30 @@ FM_DEV uint64_t evict_first_policy() {
   return p;
 }
 
-template <class E>
+template <class E, int NW = kConsumerWarps>
 struct Geometry {
   using T = typename E::Elem;
+  static constexpr int kWarps = NW;
   static constexpr int kNin = E::kNin;
-  static constexpr int kChunkBytes = kNin <= 2 ? 2 * kChunkBytesMax : (kNin <= 4 ? kChunkBytesMax : kChunkBytesMax / 2);
+  // 16 consumer warps: 32 / 16 / 8 KiB per input; other warp counts: whole
+  // 16-byte vectors for every consumer lane (2 or 1 per lane per input)
+  static constexpr int kChunkBytes =
+      NW == kConsumerWarps ? (kNin <= 2 ? 2 * kChunkBytesMax : (kNin <= 4 ? kChunkBytesMax : kChunkBytesMax / 2))
+                           : (kNin <= 2 ? 2 : 1) * 16 * 32 * NW;
   static constexpr int kChunk = kChunkBytes / (int)sizeof(T);               // elements per chunk
   static constexpr int kStagesRaw = kSmemBudget / (kChunkBytes * (kNin > 0 ? kNin : 1));
   static constexpr int kStages = kStagesRaw > 8 ? 8 : (kStagesRaw < 2 ? 2 : kStagesRaw);
   static constexpr int kSmem = kStages * kNin * kChunkBytes + 3 * kStages * 8 + 128;
   static constexpr int kW = 16 / (int)sizeof(T);                            // elements per vector
-  static constexpr int kVecPerThread = kChunk / kW / (kConsumerWarps * 32);
-  static_assert(kChunk % (kW * kConsumerWarps * 32) == 0, "chunk splits evenly over consumers");
+  static constexpr int kVecPerThread = kChunk / kW / (NW * 32);
+  static_assert(kChunk % (kW * NW * 32) == 0, "chunk splits evenly over consumers");
   static constexpr bool kOk = kNin <= 8 && kSmem <= 200 * 1024;             // fits the ring
 };
 
 // shared-memory ring: [stage][input] chunks, then full[S] / empty[S] mbarriers
-template <class E>
+template <class E, int NW = kConsumerWarps>
 struct Ring {
-  using G = Geometry<E>;
+  using G = Geometry<E, NW>;
   unsigned char *base;
   uint64_t *full, *empty;
   int64_t *cid;          // chunk held by each stage (-1: no more chunks)
@@ -105,7 +110,7 @@ struct Ring {
     if (threadIdx.x == 0) {
       for (int s = 0; s < G::kStages; ++s) {
         mbar_init(&full[s], 1);
-        mbar_init(&empty[s], kConsumerWarps);
+        mbar_init(&empty[s], NW);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -150,7 +155,7 @@ struct Ring {
     constexpr int NIN = G::kNin;
 #pragma unroll
     for (int j = 0; j < G::kVecPerThread; ++j) {
-      const int q = ctid + j * kConsumerWarps * 32;
+      const int q = ctid + j * NW * 32;
       uint4 w[NIN];
 #pragma unroll
       for (int i = 0; i < NIN; ++i) w[i] = *(const uint4 *)(chunk(s, i) + q * 16);
@@ -172,24 +177,36 @@ struct Ring {
   }
 };
 
+// Consumer warps of the bulk copy: transcendental f32 chains of <= 4 inputs
+// (sigmoid, swish, gelu: one exp / tanh per element evaluated in f64) stall on
+// the dependent FP64 chain ("wait" is the top stall at 16 warps,
+// profiles/r02/ncu_suite_sigmoid.txt), so they run 24 (800 threads with the
+// producer warp, <= 80 registers).
 template <class E>
-__global__ void __launch_bounds__(kBulkThreads, 1)
+struct CopyWarps {
+  static constexpr int v = (E::kHeavy && sizeof(typename E::Elem) == 4 && E::kNin <= 4) ? 24 : kConsumerWarps;
+};
+template <class E> constexpr int copy_bulk_threads() { return (CopyWarps<E>::v + 1) * 32; }
+
+template <class E>
+__global__ void __launch_bounds__(copy_bulk_threads<E>(), 1)
     k_copy_bulk(const __grid_constant__ fm_program P, void *out, int64_t n_elem, unsigned *counters) {
-  using G = Geometry<E>;
+  constexpr int NW = CopyWarps<E>::v;
+  using G = Geometry<E, NW>;
   using T = typename E::Elem;
   constexpr int S = G::kStages, C = G::kChunk;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Ring<E> ring(smem_raw);
+  Ring<E, NW> ring(smem_raw);
   ring.init();
   const int indep = P.reserved & 1;   // launch-window class (common.cuh)
   pdl_enter(indep);
   const int warp = threadIdx.x >> 5;
   const int64_t nfull = n_elem / C;
   unsigned *ctr = counters, *done = counters + 1;
-  if (warp == kConsumerWarps) {
+  if (warp == NW) {
     if ((threadIdx.x & 31) == 0) ring.produce(P, nfull, 0, ctr);   // all dynamic: copies are order-free
   } else {
-  const int ctid = threadIdx.x;   // 0 .. kConsumerWarps*32-1
+  const int ctid = threadIdx.x;   // 0 .. NW*32-1
   for (int64_t k = 0;; ++k) {
     const int s = (int)(k % S);
     mbar_wait(&ring.full[s], (uint32_t)((k / S) & 1));
@@ -201,7 +218,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
     T *o = (T *)out + c * C;
 #pragma unroll
     for (int j = 0; j < G::kVecPerThread; ++j) {
-      const int q = ctid + j * kConsumerWarps * 32;
+      const int q = ctid + j * NW * 32;
       if constexpr (sizeof(T) == 8) {
         uint32_t a0, a1, b0, b1;
         d2u(r[j][0], a0, a1);
@@ -217,7 +234,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   if (blockIdx.x == 0) {
     constexpr int V = E::kV;
     const int64_t base = nfull * C;
-    for (int64_t e0 = base + (int64_t)ctid * V; e0 < n_elem; e0 += (int64_t)kConsumerWarps * 32 * V) {
+    for (int64_t e0 = base + (int64_t)ctid * V; e0 < n_elem; e0 += (int64_t)NW * 32 * V) {
       Chunk ch;
       ch.base = e0;
       ch.cnt = (int)min((int64_t)V, n_elem - e0);

@@ -99,7 +99,7 @@ bool host_fast_ok(const fm_program &P, const void *out) {
 
 template <class E>
 int run_copy_bulk(const fm_program &P, void *out, int64_t n_elem, cudaStream_t s) {
-  using G = bulk::Geometry<E>;
+  using G = bulk::Geometry<E, bulk::CopyWarps<E>::v>;
   static bool attr = false;
   if (!attr) {
     FM_CHECK(cudaFuncSetAttribute(bulk::k_copy_bulk<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
@@ -111,7 +111,7 @@ int run_copy_bulk(const fm_program &P, void *out, int64_t n_elem, cudaStream_t s
   Scratch sc;
   int st = get_scratch((void *)s, 64, &sc, cl.slot);
   if (st) return st;
-  FM_CHECK(launch_pdl(bulk::k_copy_bulk<E>, dim3((unsigned)grid), dim3(bulk::kBulkThreads), G::kSmem, s, cl.P, out,
+  FM_CHECK(launch_pdl(bulk::k_copy_bulk<E>, dim3((unsigned)grid), dim3(bulk::copy_bulk_threads<E>()), G::kSmem, s, cl.P, out,
                       n_elem, sc.counters));
   FM_CHECK_LAUNCH("fused copy kernel (bulk)");
   return 0;

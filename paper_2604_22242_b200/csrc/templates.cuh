@@ -93,14 +93,14 @@ template <class A, class B> struct Heavy<Sub<A, B>> { static constexpr bool v = 
 template <class A, class B> struct Heavy<Mul<A, B>> { static constexpr bool v = Heavy<A>::v || Heavy<B>::v; };
 template <class A, class B> struct Heavy<Div<A, B>> { static constexpr bool v = Heavy<A>::v || Heavy<B>::v; };
 
-// RegTiles<Expr>::v -- stream on register tiles even beyond L2: the chains
-// whose per-element math is longest (tanh, an elementwise division) need the
-// register path's 32-40 resident warps to hide it; the bulk skeleton runs 16
-// consumer warps per SM.  Measured at 10000^2 f32 (bench.py --config suite):
-// swish 4.02 (tiles) vs 3.44 TB/s (bulk), gelu 2.03 vs 1.84, while sigmoid
-// (scalar division) 3.99 vs 4.52 and C3 6.44 vs 7.02 favour bulk.
+// RegTiles<Expr>::v -- stream on register tiles even beyond L2: a chain with
+// an elementwise division needs the register path's 32-40 resident warps to
+// hide it.  Measured at 10000^2 f32 (bench.py --config suite): swish 4.25
+// (tiles) vs 4.04 TB/s (bulk, 24 consumer warps for transcendental chains),
+// while gelu (tanh) 3.83 vs 4.04, sigmoid (scalar division) and C3 favour
+// bulk.  (With 16 bulk consumer warps tanh chains were faster on tiles too.)
 template <class X> struct RegTiles { static constexpr bool v = false; };
-template <class A> struct RegTiles<Tanh<A>> { static constexpr bool v = true; };
+template <class A> struct RegTiles<Tanh<A>> { static constexpr bool v = RegTiles<A>::v; };
 template <class A, class B> struct RegTiles<Div<A, B>> { static constexpr bool v = true; };
 template <class A> struct RegTiles<Exp<A>> { static constexpr bool v = RegTiles<A>::v; };
 template <class A> struct RegTiles<Log<A>> { static constexpr bool v = RegTiles<A>::v; };

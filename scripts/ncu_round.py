@@ -25,6 +25,8 @@ CAPS = {
     "ncu_suite_expr1": (r"k_copy_pair<.*SMul<\(int\)1, .*float", "suite", 0),
     "ncu_suite_expr2": (r"k_copy_pair<.*Log<.*float", "suite", 0),
     "ncu_suite_add32": (r"k_copy<.*In<\(int\)31>", "suite", 0),
+    "ncu_suite_sigmoid": (r"k_copy\w*<.*SDiv<.*Exp<", "suite", 0),
+    "ncu_suite_gelu": (r"k_copy\w*<.*Tanh<", "suite", 0),
 }
 
 

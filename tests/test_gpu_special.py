@@ -121,3 +121,29 @@ def test_transposed_copy_with_special_values(gpu_ctx):
     assert np.array_equal(np.isnan(got), np.isnan(want))
     ok = ~np.isnan(want)
     assert np.array_equal(got[ok].view(np.uint32), want[ok].view(np.uint32))
+
+
+@pytest.mark.parametrize("name", ["sigmoid", "swish", "gelu", "softplus"])
+def test_transcendental_chains_at_bulk_scale(gpu_ctx, name):
+    """The suite's transcendental members run the bulk-staged copy with 24
+    consumer warps (bulk.cuh CopyWarps); a ragged 2^22 + 37 elements against
+    the oracle (f32 exp / tanh correctly rounded, every node rounded to f32)."""
+    import math
+    n = (1 << 22) + 37
+    a = np.random.default_rng(21).uniform(-12, 12, n).astype(np.float32).reshape(-1, 1)
+    a[:9, 0] = [0.0, -0.0, np.inf, -np.inf, np.nan, 88.0, -88.0, 1e-30, -1e-30]
+    A = fm.from_array(a, ctx=gpu_ctx)
+    exprs = {
+        "sigmoid": lambda X: 1 / (1 + fm.exp(-X)),
+        "swish": lambda X: X / (1 + fm.exp(-1.0 * X)),
+        "gelu": lambda X: (X / 2) * (1 + fm.tanh(math.sqrt(2.0 / 3.14159265358979) * (X + 0.044715 * (X ** 3)))),
+        "softplus": lambda X: fm.log(1 + fm.exp(X)),
+    }
+    e = exprs[name](A)
+    got = e.eval().to_numpy()
+    want = orc.materialize(e.node, {A.mat_id: a})
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    ok = ~np.isnan(want)
+    assert orc.max_ulp(got[ok], want[ok]) <= 2, name
+    diff = np.count_nonzero(got[ok].view(np.uint32) != want[ok].view(np.uint32))
+    assert diff <= n // 100_000, (name, diff)
