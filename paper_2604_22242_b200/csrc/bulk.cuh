@@ -180,11 +180,12 @@ struct Ring {
 // Consumer warps of the bulk copy: transcendental f32 chains of <= 4 inputs
 // (sigmoid, swish, gelu: one exp / tanh per element evaluated in f64) stall on
 // the dependent FP64 chain ("wait" is the top stall at 16 warps,
-// profiles/r02/ncu_suite_sigmoid.txt), so they run 24 (800 threads with the
-// producer warp, <= 80 registers).
+// profiles/r02/ncu_suite_sigmoid.txt), so they run 31 (1024 threads with the
+// producer warp, <= 64 registers, no spills): expr3 3.03 -> 3.72 TB/s (24
+// warps: 3.39), sigmoid 4.74 -> 4.86, C3 unchanged.
 template <class E>
 struct CopyWarps {
-  static constexpr int v = (E::kHeavy && sizeof(typename E::Elem) == 4 && E::kNin <= 4) ? 24 : kConsumerWarps;
+  static constexpr int v = (E::kHeavy && sizeof(typename E::Elem) == 4 && E::kNin <= 4) ? 31 : kConsumerWarps;
 };
 template <class E> constexpr int copy_bulk_threads() { return (CopyWarps<E>::v + 1) * 32; }
 
