@@ -28,6 +28,10 @@ LABELS = {
     "c5_gemm_f32": "ncu_c5f32_gemm",
     "expr1": "ncu_suite_expr1",
     "expr2": "ncu_suite_expr2",
+    "expr3": "ncu_suite_expr3",
+    "sigmoid": "ncu_suite_sigmoid",
+    "gelu": "ncu_suite_gelu",
+    "add32N": "ncu_suite_add32",
 }
 
 

@@ -27,6 +27,7 @@ CAPS = {
     "ncu_suite_add32": (r"k_copy<.*In<\(int\)31>", "suite", 0),
     "ncu_suite_sigmoid": (r"k_copy\w*<.*SDiv<.*Exp<", "suite", 0),
     "ncu_suite_gelu": (r"k_copy\w*<.*Tanh<", "suite", 0),
+    "ncu_suite_expr3": (r"k_copy\w*<.*CvtU32<", "suite", 0),
 }
 
 
