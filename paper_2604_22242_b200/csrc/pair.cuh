@@ -121,17 +121,12 @@ FM_DEV uint2 lds64(uint32_t a) {
   return r;
 }
 
-// Heavy<E>: a template whose per-element math is long (a transcendental).
-template <class E, bool VM = E::kIsVm>
-struct HeavyT { static constexpr bool v = false; };
-template <class E>
-struct HeavyT<E, false> { static constexpr bool v = E::kHeavy; };
-
 // Thread geometry: 32 lanes = the 32 tile columns; 32 / V consumer warps
-// cover the rows of one output tile.  Light programs: every consumer thread
-// evaluates its chunk of BOTH output tiles of the pair (per-pair costs
-// amortised over 2 V elements); heavy ones (a transcendental) split the two
-// tiles over two warp groups, so a stage feeds twice the warps.  One more
+// cover the rows of one output tile.  Direct-path programs split the pair's
+// two output tiles over two warp groups, so a stage feeds twice the warps
+// (heavy chains: the FP64 transcendental latency; light ones too since the
+// kernel runs at 8 consumer warps per SM otherwise -- expr1 +2-3 % at
+// 10000^2 / 8192^2); VM programs evaluate both tiles per thread.  One more
 // warp is the producer: it waits for a stage to be released, then stages
 // the next pair into it (warp-specialised ring, no block-wide barrier in the
 // loop).
@@ -139,7 +134,7 @@ template <class E>
 struct Geo {
   static constexpr int V = E::kV;
   static constexpr int kWarpsPerTile = kTile / V;
-  static constexpr int kGroups = (Direct<E>::v && HeavyT<E>::v) ? 2 : 1;
+  static constexpr int kGroups = Direct<E>::v ? 2 : 1;
   static constexpr int kConsumerWarps = kWarpsPerTile * kGroups;
   static constexpr int kThreads = 32 * (kConsumerWarps + 1);
 };
