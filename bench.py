@@ -966,6 +966,34 @@ def cpu_leg(cfg: Config, scale: float, steps=3, warmup=1) -> dict:
             "cpu_model": cpu_model(), "nproc": os.cpu_count()}
 
 
+def dominant_kernel(labels, kwork, per_kernel, steps_ms) -> dict:
+    """The roofline's kernel: launches of one kernel ("c1_copy_f32[0..5]")
+    form a family, and the family with the largest share of the
+    instrumented step dominates.  Its mean launch duration comes from the
+    events between launches, except when every launch of the step belongs
+    to it: then the timed step's own events over the launch count give it
+    (no events between the launches, which cost ~6 us each).
+
+    labels / kwork: per launch slot; per_kernel[i]: slot i's event-timed
+    duration (ms) in each instrumented step; steps_ms: the timed steps."""
+    steps = len(per_kernel[0])
+    share = [sum(v) for v in per_kernel]
+    fam = [l.split("[")[0] for l in labels]
+    fams = sorted({f for f, w in zip(fam, kwork) if w})
+    fshare = {f: sum(s for s, g in zip(share, fam) if g == f) for f in fams}
+    fwork = {f: sum(w for w, g in zip(kwork, fam) if g == f) for f in fams}
+    fcount = {f: sum(1 for g in fam if g == f) for f in fams}
+    dfam = max(fams, key=lambda f: fshare[f])
+    step_mean = statistics.fmean(steps_ms)
+    if len(set(fam)) == 1:
+        mean_launch = step_mean / fcount[dfam]
+    else:
+        mean_launch = fshare[dfam] / (steps * fcount[dfam])
+    return {"kernel": dfam, "first_label": labels[fam.index(dfam)], "launches_per_step": fcount[dfam],
+            "mean_launch_ms": mean_launch, "work_per_launch": fwork[dfam] / fcount[dfam],
+            "work_per_step": fwork[dfam], "share_of_step_ms": step_mean * fshare[dfam] / sum(share)}
+
+
 def measure(run: Run, cfg: Config, steps: int, warmup: int, with_cpu: bool, with_e2e: bool,
             use_graph: bool = True) -> dict:
     fm, nat, backend, p = run.fm, run.nat, run.backend, run.p
@@ -1074,28 +1102,13 @@ def measure(run: Run, cfg: Config, steps: int, warmup: int, with_cpu: bool, with
     work_all = p.sum(sum(kwork))
     value = work_all / (ms_per_step * 1e-3) / scale
     peaks = measured_peaks()
-    means = [statistics.fmean(v) for v in per_kernel]
-    share = [sum(v) for v in per_kernel]
-    # launches of one kernel ("c1_copy_f32[0..5]") form a family: the
-    # dominant kernel is the family with the largest share of the step
-    fam = [l.split("[")[0] for l in labels]
-    fams = sorted({f for f, w in zip(fam, kwork) if w})
-    fshare = {f: sum(s for s, g in zip(share, fam) if g == f) for f in fams}
-    fwork = {f: sum(w for w, g in zip(kwork, fam) if g == f) for f in fams}
-    fcount = {f: sum(1 for g in fam if g == f) for f in fams}
-    dfam = max(fams, key=lambda f: fshare[f])
-    step_mean = statistics.fmean(steps_ms)
-    if len(set(fam)) == 1:
-        # the whole step is this kernel: its launches' mean duration is the
-        # event-timed step over the launch count
-        mean_launch = step_mean / fcount[dfam]
-    else:
-        mean_launch = fshare[dfam] / (steps * fcount[dfam])
-    work_launch = fwork[dfam] / fcount[dfam]
+    dk = dominant_kernel(labels, kwork, per_kernel, steps_ms)
+    dfam, mean_launch, work_launch = dk["kernel"], dk["mean_launch_ms"], dk["work_per_launch"]
     achieved = work_launch / (mean_launch * 1e-3) / scale
-    in_step = fwork[dfam] / (step_mean * fshare[dfam] / sum(share) * 1e-3) / scale
-    dom = fam.index(dfam)
-    common = {"kernel": dfam, "launches_per_step": fcount[dfam], "achieved": round(achieved, 1),
+    in_step = dk["work_per_step"] / (dk["share_of_step_ms"] * 1e-3) / scale
+    dom = labels.index(dk["first_label"])
+    means = [statistics.fmean(v) for v in per_kernel]
+    common = {"kernel": dfam, "launches_per_step": dk["launches_per_step"], "achieved": round(achieved, 1),
               "traffic": ncu_traffic(labels[dom]),
               "mean_launch_us": round(mean_launch * 1e3, 2), "achieved_in_timed_steps": round(in_step, 1),
               "timing": TIMING_NOTE}

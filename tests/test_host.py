@@ -274,3 +274,23 @@ def test_plan_and_bind_memo():
     k = ctx.cache.lookup(p1.steps[0].signature)
     with pytest.raises(BackendError):                     # memo never bypasses the UAF check
         b.launch(k, [Z.handle, 64, 32, X.handle, 64, 32, old, 64, 32, 2.0], (64, 32))
+
+
+def test_bench_dominant_kernel_families():
+    """bench.py's roofline kernel: launches of one kernel form a family; a
+    step made only of that family takes its launch time from the step events
+    (no events between launches); a mixed step from the instrumented pass."""
+    import bench
+    # C1-like: six launches of one kernel, instrumented times inflated by events
+    labels = [f"c1[{i}]" for i in range(6)]
+    per = [[0.036, 0.036] for _ in range(6)]
+    d = bench.dominant_kernel(labels, [100] * 6, per, [0.18, 0.18])
+    assert d["kernel"] == "c1" and d["launches_per_step"] == 6
+    assert abs(d["mean_launch_ms"] - 0.03) < 1e-12 and d["work_per_launch"] == 100
+    # mixed step: the family with the largest instrumented share wins
+    labels = ["a", "b[0]", "b[1]", "gather"]
+    per = [[1.0, 1.0], [0.8, 0.8], [0.8, 0.8], [0.1, 0.1]]
+    d = bench.dominant_kernel(labels, [10, 20, 20, 0], per, [2.5, 2.5])
+    assert d["kernel"] == "b" and d["first_label"] == "b[0]" and d["launches_per_step"] == 2
+    assert abs(d["mean_launch_ms"] - 0.8) < 1e-12 and d["work_per_step"] == 40
+    assert abs(d["share_of_step_ms"] - 2.5 * 3.2 / 5.4) < 1e-12
